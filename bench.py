@@ -1,0 +1,406 @@
+#!/usr/bin/env python
+"""Benchmark of the S2 sparse-sketch reduce on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config resnet50]
+
+One step = one full reduce of one synthetic gradient per rank: compress (bitmap +
+compaction + count-sketch insert) -> sketch all-reduce + bitmap all-gather/OR
+(N > 1, NCCL over NVLink) -> median decode (÷N) into a dense fp32 gradient.
+
+Prints ONE JSON line (rank 0).  ``value`` = whole-job dense-equivalent GB/s =
+N * 4*d / t_reduce (t = max over ranks, CUDA events, K steps); ``ms_per_step``
+= t_reduce.  ``e2e`` repeats the measurement through the same C-ABI call with
+pinned HOST buffers, H2D of the gradient and D2H of the result inside the timed
+region.  ``--impl reference`` times the CPU reference path (the NumPy oracle
+port of sketchgrad.sparse, bit-identical to the as-shipped reference) on the
+host cores instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "dense-equivalent gradient GB/s reduced per GPU and ms/reduce at 1/2/4/8 B200"
+CONFIGS = {
+    # configs[1] of BASELINE.json: the headline (fits one GPU)
+    "resnet50": dict(dim=25_600_000, alpha=0.01, rows=3, cols=262_144, label="ResNet-50-sized 25.6M fp32, 99% sparse"),
+    "bert": dict(dim=110_000_000, alpha=0.05, rows=5, cols=1_048_576, label="BERT-base-sized 110M fp32, 95% sparse"),
+    "bert_np2": dict(dim=110_000_000, alpha=0.05, rows=5, cols=1_000_000, label="BERT-base 110M, 95%, 5x1,000,000"),
+    "gpt2m_90": dict(dim=355_000_000, alpha=0.10, rows=3, cols=1_048_576, label="GPT-2-medium 355M, 90% sparse"),
+    "gpt2m_999": dict(dim=355_000_000, alpha=0.001, rows=3, cols=262_144, label="GPT-2-medium 355M, 99.9% sparse"),
+    "oracle1m": dict(dim=1_000_000, alpha=0.01, rows=3, cols=16_384, label="1M fp32, 99% sparse (configs[0])"),
+}
+N_ROTATE = 4  # distinct gradient buffers cycled through: N_ROTATE * 4d bytes > 126 MB L2
+HBM_FALLBACK = 6650.0  # GB/s, B200_PROFILING.md fallback
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return HBM_FALLBACK, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled in the background (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.marks = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=timestamp,clocks.sm,clocks.max.sm,power.draw,utilization.gpu,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append((time.time(), [x.strip() for x in line.split(",")]))
+
+    def mark(self, name):
+        self.marks.append((name, time.time()))
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except Exception:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        marks = dict(self.marks)
+        t0, t1 = marks.get("load_start", 0), marks.get("load_end", time.time())
+        sm, mx, reasons, in_load = [], 0.0, set(), 0
+        for ts, r in self.rows:
+            try:
+                smv, mxv = float(r[1]), float(r[2])
+            except (ValueError, IndexError):
+                continue
+            mx = max(mx, mxv)
+            if t0 <= ts <= t1:
+                in_load += 1
+                sm.append(smv)
+                for n, v in zip(names, r[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+        if not sm:  # region shorter than the sampling period: use every sample of the run
+            for ts, r in self.rows:
+                try:
+                    sm.append(float(r[1]))
+                except (ValueError, IndexError):
+                    pass
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples_under_load": in_load, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------- reference
+
+
+def reference_arm(args, cfg):
+    """CPU reference: oracle port of sketchgrad.sparse (compress per rank in W processes,
+    merge, decompress), on the host cores.  Rank 0 only under torchrun."""
+    from oracle import s2_oracle as o
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    W = args.gpus
+    d, rows, cols = cfg["dim"], cfg["rows"], cfg["cols"]
+    grads = [o.synthetic_gradient(d, cfg["alpha"], r) for r in range(W)]
+
+    def one_step(pool):
+        if pool is None:
+            ps = [o.compress(grads[0], grads[0] != 0, rows, cols, 0)]
+        else:
+            ps = pool.map(_ref_compress, [(r, rows, cols) for r in range(W)])
+        m = o.merge(ps)
+        return o.decompress(m)
+
+    pool = None
+    if W > 1:
+        import multiprocessing as mp
+
+        global _REF_GRADS
+        _REF_GRADS = grads
+        pool = mp.get_context("fork").Pool(W)
+    for _ in range(args.warmup):
+        one_step(pool)
+    t0 = time.perf_counter()
+    done = 0
+    while done < args.steps:
+        one_step(pool)
+        done += 1
+        if time.perf_counter() - t0 > args.ref_budget and done >= 3:
+            break  # bounded sample: the run must finish within a few minutes
+    dt = (time.perf_counter() - t0) / done
+    if pool is not None:
+        pool.close()
+    value = W * 4 * d / dt / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": W,
+        "steps": done, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": _config_json(args, cfg),
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": W, "kind": "port",
+                         "sample": f"full workload per step: {W} rank compress (one process each) + merge + "
+                                   f"decompress of {d} elements; numpy {np.__version__}; host has "
+                                   f"{os.cpu_count()} cores"},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+_REF_GRADS = None
+
+
+def _ref_compress(a):
+    from oracle import s2_oracle as o
+
+    r, rows, cols = a
+    g = _REF_GRADS[r]
+    return o.compress(g, g != 0, rows, cols, 0)
+
+
+def cpu_baseline(cfg, budget_s=10.0):
+    """Oracle port timed on this host (rank 0, N=1): compress + merge + decompress of one gradient."""
+    from oracle import s2_oracle as o
+
+    d = cfg["dim"]
+    g = o.synthetic_gradient(d, cfg["alpha"], 0)
+    n, t0 = 0, time.perf_counter()
+    while True:
+        p = o.compress(g, g != 0, cfg["rows"], cfg["cols"], 0)
+        o.decompress(o.merge([p]))
+        n += 1
+        if time.perf_counter() - t0 > budget_s or n >= 50:
+            break
+    dt = (time.perf_counter() - t0) / n
+    return {"value": round(4 * d / dt / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "port",
+            "sample": f"{n} full reduces (W=1) of the {d}-element workload in {time.perf_counter() - t0:.1f}s; "
+                      f"numpy {np.__version__} single-threaded; host has {os.cpu_count()} cores"}
+
+
+def _config_json(args, cfg):
+    return {"workload": f"{args.config}: {cfg['label']}, sketch {cfg['rows']}x{cfg['cols']}, W={args.gpus}",
+            "dim": cfg["dim"], "nnz_per_rank": int(round(cfg["alpha"] * cfg["dim"])), "rows": cfg["rows"],
+            "cols": cfg["cols"], "world": args.gpus, "parallelism": f"dp{args.gpus}",
+            "l2": f"inputs rotate over {N_ROTATE} gradient buffers ({N_ROTATE * 4 * cfg['dim'] / 1e6:.0f} MB > 126 MB L2)"}
+
+
+# --------------------------------------------------------------------- ours
+
+
+def ours(args, cfg):
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    world = args.gpus
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2110_02140_b200 as s2
+    from paper_2110_02140_b200._lib import check, lib, ptr
+    from oracle import s2_oracle as o  # input generation only (same bytes the oracle sees)
+
+    d, rows, cols = cfg["dim"], cfg["rows"], cfg["cols"]
+    red = s2.S2Reducer(d, rows=rows, cols=cols, seed=0, world=world, rank=rank)
+    grads = [torch.from_numpy(o.synthetic_gradient(d, cfg["alpha"], rank, base_seed=1234 + 1000 * k)).cuda()
+             for k in range(N_ROTATE)]
+    outs = [torch.empty(d, dtype=torch.float32, device="cuda") for _ in range(N_ROTATE)]
+    stream = torch.cuda.current_stream()
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    h = red.plan.handle
+    cnt = ptr(red.counters)
+    gp = [ptr(g) for g in grads]
+    op = [ptr(x) for x in outs]
+
+    def step(i):
+        check(lib.s2_reduce(h, gp[i % N_ROTATE], op[i % N_ROTATE], cnt, sp))
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    clocks = ClockSampler(local) if rank == 0 or True else None
+    clocks.start()
+    time.sleep(0.2)
+    clocks.mark("load_start")
+    for i in range(args.warmup):
+        step(i)
+    # soak: keep the GPU busy ~0.3 s before timing so clocks settle (extra untimed warm-up)
+    barrier()
+    t_soak = time.time()
+    i = 0
+    while time.time() - t_soak < 0.3:
+        for _ in range(50):
+            step(i)
+            i += 1
+        torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        step(i)
+    e1.record(stream)
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+
+    # per-phase durations (same launches, events between them) for the roofline
+    counters = red.counters
+    tab = torch.empty(rows * cols, dtype=torch.float32, device="cuda")
+    bm = torch.empty(-(-d // 32) + 4, dtype=torch.int32, device="cuda")
+    un = torch.empty_like(bm)
+    phases = {"compress": 0.0, "aggregate": 0.0, "decode": 0.0}
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    nph = max(args.steps, 20)
+    barrier()
+    for i in range(nph):
+        ev[0].record(stream)
+        check(lib.s2_compress(h, gp[i % N_ROTATE], ptr(bm), ptr(tab), 0, cnt, sp))
+        ev[1].record(stream)
+        if world > 1:
+            check(lib.s2_aggregate(h, ptr(tab), ptr(bm), ptr(un), sp))
+        ev[2].record(stream)
+        check(lib.s2_decode(h, ptr(un) if world > 1 else ptr(bm), ptr(tab), world, op[i % N_ROTATE], sp))
+        ev[3].record(stream)
+        ev[3].synchronize()
+        phases["compress"] += ev[0].elapsed_time(ev[1])
+        phases["aggregate"] += ev[1].elapsed_time(ev[2])
+        phases["decode"] += ev[2].elapsed_time(ev[3])
+    phases = {k: max_over_ranks(v / nph) for k, v in phases.items()}
+
+    # e2e: pinned host gradient in, pinned host result out, copies inside the timed region
+    hg = [torch.empty(d, dtype=torch.float32, pin_memory=True) for _ in range(2)]
+    for k in range(2):
+        hg[k].copy_(grads[k].cpu())
+    ho = torch.empty(d, dtype=torch.float32, pin_memory=True)
+    dg = torch.empty(d, dtype=torch.float32, device="cuda")
+    do = torch.empty(d, dtype=torch.float32, device="cuda")
+    ke = max(3, min(args.steps, 50))
+    for i in range(2):
+        dg.copy_(hg[i % 2], non_blocking=True)
+        red.reduce(dg, out=do)
+        ho.copy_(do, non_blocking=True)
+    barrier()
+    e0.record(stream)
+    for i in range(ke):
+        dg.copy_(hg[i % 2], non_blocking=True)
+        red.reduce(dg, out=do)
+        ho.copy_(do, non_blocking=True)
+    e1.record(stream)
+    barrier()
+    clocks.mark("load_end")
+    ms_e2e = max_over_ranks(e0.elapsed_time(e1) / ke)
+    clk = clocks.stop()
+
+    red.check_finite()
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    hbm_peak, peak_kind = peaks()
+    B = 4 * d
+    words_bytes = 4 * (-(-d // 32))
+    table_bytes = 4 * rows * cols
+    alg = {"compress": B + words_bytes + table_bytes, "decode": words_bytes + table_bytes + B}
+    dom = max(("compress", "decode"), key=lambda k: phases[k])
+    ach = alg[dom] / (phases[dom] * 1e-3) / 1e9
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tfile):
+        traffic = json.load(open(tfile)).get(f"{args.config}:{dom}")
+    phase_out = {}
+    for k in ("compress", "decode"):
+        a = alg[k] / (phases[k] * 1e-3) / 1e9
+        phase_out[k] = {"ms": round(phases[k], 5), "GB/s": round(a, 1), "frac": round(a / hbm_peak, 4),
+                        "algorithmic_bytes": alg[k]}
+    if world > 1:
+        bus = 2 * (world - 1) / world * table_bytes + (world - 1) / world * world * words_bytes
+        phase_out["aggregate"] = {"ms": round(phases["aggregate"], 5),
+                                  "bus_GB/s": round(bus / (phases["aggregate"] * 1e-3) / 1e9, 1),
+                                  "bus_bytes": bus}
+    value = world * B / (ms * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 5), "per_gpu_GBps": round(B / (ms * 1e-3) / 1e9, 2),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": _config_json(args, cfg),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
+                     "frac": round(ach / hbm_peak, 4), "traffic": traffic, "peak_kind": peak_kind,
+                     "bytes_per_launch": alg[dom]},
+        "phases": phase_out,
+        "e2e": {"value": round(world * B / (ms_e2e * 1e-3) / 1e9, 3), "unit": "GB/s", "ms_per_step": round(ms_e2e, 4),
+                "h2d_bytes_per_step": B, "d2h_bytes_per_step": B,
+                "path": "S2Reducer.reduce (C-ABI s2_reduce) with pinned host buffers"},
+        "gpu_launches": args.steps * (3 if world > 1 else 2),
+        "clocks": clk,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_budget)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="resnet50", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--ref-budget", type=float, default=120.0, help="max seconds of timed reference steps")
+    args = ap.parse_args()
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws != args.gpus and "WORLD_SIZE" in os.environ:
+        args.gpus = ws
+    args.warmup = max(args.warmup, 3)
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        reference_arm(args, cfg)
+    else:
+        ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

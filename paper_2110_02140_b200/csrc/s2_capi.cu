@@ -1,0 +1,361 @@
+// s2_capi.cu — the C ABI of libs2.so (include/s2.h): plans, host hashing,
+// stream-ordered device ops and the NCCL/NVLink distributed reduce.
+#include <nccl.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "s2.h"
+#include "s2_common.cuh"
+#include "s2_kernels.h"
+
+using s2::HashParams;
+using s2::Plan;
+
+struct s2_plan {
+  Plan p;
+  // distributed state
+  int world = 1;
+  int rank = 0;
+  ncclComm_t comm = nullptr;
+  // plan-owned scratch for s2_reduce / s2_aggregate
+  float* table = nullptr;
+  uint32_t* bitmap = nullptr;
+  uint32_t* unionmap = nullptr;
+  uint32_t* gather = nullptr;  // world * words (all-gather landing buffer)
+  unsigned long long* counters = nullptr;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(S2_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define S2_CUDA(call, what)                      \
+  do {                                           \
+    cudaError_t e_ = (call);                     \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+  } while (0)
+
+#define S2_NCCL(call, what)                                                         \
+  do {                                                                              \
+    ncclResult_t r_ = (call);                                                       \
+    if (r_ != ncclSuccess) return fail(S2_ENCCL, "%s: %s", what, ncclGetErrorString(r_)); \
+  } while (0)
+
+uint64_t derive(const uint64_t* parts, int n) {  // core.py:44-54
+  uint64_t acc = s2::kDeriveInit;
+  for (int k = 0; k < n; ++k) acc = s2::mix64(acc + parts[k] * s2::kGolden);
+  return acc;
+}
+
+int build_hash(uint64_t seed, int rows, int64_t cols, int injective, HashParams* hp) {
+  if (rows < 1 || cols < 1)
+    return fail(S2_EINVAL, "rows and cols must be >= 1, got %dx%lld", rows, (long long)cols);
+  if (rows > S2_MAX_ROWS) return fail(S2_EINVAL, "rows must be <= %d, got %d", S2_MAX_ROWS, rows);
+  if (cols >= (int64_t)1 << 32) return fail(S2_EINVAL, "cols must be < 2^32, got %lld", (long long)cols);
+  memset(hp, 0, sizeof *hp);
+  hp->rows = rows;
+  hp->cols = (uint32_t)cols;
+  for (int j = 0; j < rows; ++j) {
+    const uint64_t parts[2] = {seed, (uint64_t)j};
+    hp->seed[j] = derive(parts, 2);  // sketch.py:96-99
+  }
+  if (injective) {
+    hp->mode = s2::kInjective;
+  } else if ((cols & (cols - 1)) == 0) {
+    hp->mode = s2::kPow2;
+  } else {
+    int l = 0;
+    while (((int64_t)1 << l) < cols) ++l;  // 2^(l-1) < cols < 2^l
+    const unsigned __int128 num = (unsigned __int128)1 << (63 + l);
+    hp->magic = (uint64_t)(num / (uint64_t)cols) + 1u;  // ceil: cols never divides 2^(63+l)
+    hp->shift = (uint32_t)(l - 1);
+    hp->mode = s2::kMagic;
+  }
+  return S2_OK;
+}
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+extern "C" {
+
+const char* s2_last_error(void) { return g_err.c_str(); }
+int s2_abi_version(void) { return 1; }
+
+uint64_t s2_mix64(uint64_t x) { return s2::mix64(x); }
+
+uint64_t s2_derive_seed(const uint64_t* parts, int nparts) { return derive(parts, nparts); }
+
+int s2_row_seeds(uint64_t seed, int rows, uint64_t* out) {
+  if (rows < 1 || rows > S2_MAX_ROWS) return fail(S2_EINVAL, "rows must be in [1, %d]", S2_MAX_ROWS);
+  for (int j = 0; j < rows; ++j) {
+    const uint64_t parts[2] = {seed, (uint64_t)j};
+    out[j] = derive(parts, 2);
+  }
+  return S2_OK;
+}
+
+int s2_hash_host(uint64_t row_seed, const int64_t* idx, int64_t n, int64_t cols,
+                 int64_t* buckets_out, int8_t* signs_out) {
+  HashParams hp;
+  int rc = build_hash(0, 1, cols, 0, &hp);
+  if (rc) return rc;
+  for (int64_t k = 0; k < n; ++k) {
+    const uint64_t w = s2::mix64(row_seed + s2::index_term((uint64_t)idx[k]));
+    if (buckets_out) buckets_out[k] = s2::bucket_of(w, hp);
+    if (signs_out) signs_out[k] = (w >> 63) ? -1 : 1;
+  }
+  return S2_OK;
+}
+
+int s2_plan_create(int64_t dim, int64_t num_blocks, int rows, int64_t cols, uint64_t seed,
+                   int injective, s2_plan** out) {
+  if (out == nullptr) return fail(S2_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (dim < 1) return fail(S2_EINVAL, "dim must be >= 1, got %lld", (long long)dim);
+  if (num_blocks < 1 || num_blocks > dim)
+    return fail(S2_EINVAL, "num_blocks must be in [1, dim=%lld], got %lld", (long long)dim,
+                (long long)num_blocks);
+  if (dim >= ((int64_t)1 << 32) - 1)
+    return fail(S2_EINVAL, "dim must be < 2^32 - 1 on the GPU path, got %lld", (long long)dim);
+  HashParams hp;
+  int rc = build_hash(seed, rows, cols, injective, &hp);
+  if (rc) return rc;
+  if (injective && cols < dim) {
+    // HashMapping(injective) raises only when a selected index >= buckets (core.py:131-135);
+    // the Python layer performs that check, the kernels never index past cols.
+  }
+  s2_plan* p = new s2_plan();
+  p->p.dim = dim;
+  p->p.num_blocks = num_blocks;
+  p->p.block_size = (dim + num_blocks - 1) / num_blocks;
+  p->p.words = (num_blocks + 31) / 32;
+  p->p.seed = seed;
+  p->p.injective = injective;
+  p->p.hp = hp;
+  *out = p;
+  return S2_OK;
+}
+
+static void free_scratch(s2_plan* p) {
+  cudaFree(p->table);
+  cudaFree(p->bitmap);
+  cudaFree(p->unionmap);
+  cudaFree(p->gather);
+  cudaFree(p->counters);
+  p->table = nullptr;
+  p->bitmap = p->unionmap = p->gather = nullptr;
+  p->counters = nullptr;
+}
+
+void s2_plan_destroy(s2_plan* plan) {
+  if (!plan) return;
+  if (plan->comm) ncclCommDestroy(plan->comm);
+  free_scratch(plan);
+  delete plan;
+}
+
+int64_t s2_plan_bitmap_words(const s2_plan* plan) { return plan ? plan->p.words : -1; }
+int64_t s2_plan_block_size(const s2_plan* plan) { return plan ? plan->p.block_size : -1; }
+int s2_plan_world(const s2_plan* plan) { return plan ? plan->world : -1; }
+
+int s2_compress(const s2_plan* plan, const float* g, uint32_t* bitmap, float* table, int mask_mode,
+                uint64_t* counters, void* stream) {
+  if (!plan || !g || !bitmap || !table || !counters) return fail(S2_EINVAL, "NULL argument to s2_compress");
+  if (mask_mode != S2_MASK_NONZERO && mask_mode != S2_MASK_GIVEN)
+    return fail(S2_EINVAL, "unknown mask mode %d", mask_mode);
+  if (reinterpret_cast<uintptr_t>(g) & 15) return fail(S2_EINVAL, "gradient must be 16-byte aligned");
+  S2_CUDA(s2::launch_compress(plan->p, g, bitmap, table, reinterpret_cast<unsigned long long*>(counters),
+                              mask_mode, as_stream(stream)),
+          "s2_compress");
+  return S2_OK;
+}
+
+int s2_decode(const s2_plan* plan, const uint32_t* bitmap, const float* table, int workers, float* out,
+              void* stream) {
+  if (!plan || !bitmap || !table || !out) return fail(S2_EINVAL, "NULL argument to s2_decode");
+  if (workers < 1) return fail(S2_EINVAL, "workers must be >= 1");  // sparse.py:208-209
+  if (reinterpret_cast<uintptr_t>(out) & 15) return fail(S2_EINVAL, "output must be 16-byte aligned");
+  S2_CUDA(s2::launch_decode(plan->p, bitmap, table, workers, out, as_stream(stream)), "s2_decode");
+  return S2_OK;
+}
+
+int s2_bitmap_or(int64_t words, const uint32_t* stacked, int nmasks, uint32_t* out, void* stream) {
+  if (nmasks < 1) return fail(S2_EINVAL, "nothing to merge");  // sparse.py:177-178
+  S2_CUDA(s2::launch_bitmap_or(words, stacked, nmasks, out, as_stream(stream)), "s2_bitmap_or");
+  return S2_OK;
+}
+
+int s2_table_sum(int64_t cells, const float* stacked, int ntables, float* out, void* stream) {
+  if (ntables < 1) return fail(S2_EINVAL, "nothing to merge");
+  S2_CUDA(s2::launch_table_sum(cells, stacked, ntables, out, as_stream(stream)), "s2_table_sum");
+  return S2_OK;
+}
+
+int s2_selected_count(const s2_plan* plan, const uint32_t* bitmap, uint64_t* counters, void* stream) {
+  if (!plan || !bitmap || !counters) return fail(S2_EINVAL, "NULL argument to s2_selected_count");
+  S2_CUDA(s2::launch_selected_count(plan->p, bitmap, reinterpret_cast<unsigned long long*>(counters),
+                                    as_stream(stream)),
+          "s2_selected_count");
+  return S2_OK;
+}
+
+int64_t s2_compact_scratch_bytes(const s2_plan* plan) {
+  return plan ? s2::compact_scratch_bytes(plan->p) : -1;
+}
+
+int s2_compact(const s2_plan* plan, const uint32_t* bitmap, const float* g, int64_t* idx_out,
+               float* val_out, int64_t* count, void* scratch, void* stream) {
+  if (!plan || !bitmap || !idx_out || !count || !scratch)
+    return fail(S2_EINVAL, "NULL argument to s2_compact");
+  if (g && (reinterpret_cast<uintptr_t>(g) & 15)) return fail(S2_EINVAL, "gradient must be 16-byte aligned");
+  S2_CUDA(s2::launch_compact(plan->p, bitmap, g, idx_out, g ? val_out : nullptr, count, scratch,
+                             as_stream(stream)),
+          "s2_compact");
+  return S2_OK;
+}
+
+int s2_sketch_insert(const s2_plan* plan, const int64_t* idx, const float* vals, int64_t n, float* table,
+                     void* stream) {
+  if (!plan || (n > 0 && (!idx || !vals || !table))) return fail(S2_EINVAL, "NULL argument to s2_sketch_insert");
+  S2_CUDA(s2::launch_pairs(plan->p, idx, vals, n, table, nullptr, as_stream(stream)), "s2_sketch_insert");
+  return S2_OK;
+}
+
+int s2_sketch_query(const s2_plan* plan, const int64_t* idx, int64_t n, const float* table, float* out,
+                    void* stream) {
+  if (!plan || (n > 0 && (!idx || !table || !out))) return fail(S2_EINVAL, "NULL argument to s2_sketch_query");
+  S2_CUDA(s2::launch_pairs(plan->p, idx, nullptr, n, table, out, as_stream(stream)), "s2_sketch_query");
+  return S2_OK;
+}
+
+// ------------------------------------------------------------ distributed
+
+int s2_nccl_unique_id(void* out) {
+  ncclUniqueId id;
+  S2_NCCL(ncclGetUniqueId(&id), "ncclGetUniqueId");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  memcpy(out, &id, sizeof id);
+  return S2_OK;
+}
+
+static int ensure_scratch(s2_plan* p) {
+  if (p->table) return S2_OK;
+  const size_t cells = (size_t)p->p.hp.rows * p->p.hp.cols;
+  const size_t wb = sizeof(uint32_t) * ((size_t)p->p.words + 4);
+  S2_CUDA(cudaMalloc(&p->table, cells * sizeof(float)), "cudaMalloc(table)");
+  S2_CUDA(cudaMalloc(&p->bitmap, wb), "cudaMalloc(bitmap)");
+  S2_CUDA(cudaMalloc(&p->unionmap, wb), "cudaMalloc(union)");
+  S2_CUDA(cudaMalloc(&p->counters, sizeof(unsigned long long) * S2_NUM_COUNTERS), "cudaMalloc(counters)");
+  if (p->world > 1)
+    S2_CUDA(cudaMalloc(&p->gather, sizeof(uint32_t) * (size_t)p->p.words * p->world), "cudaMalloc(gather)");
+  return S2_OK;
+}
+
+int s2_comm_init(s2_plan* plan, int world, int rank, const void* unique_id) {
+  if (!plan) return fail(S2_EINVAL, "NULL plan");
+  if (world < 1 || rank < 0 || rank >= world) return fail(S2_EINVAL, "bad world/rank %d/%d", world, rank);
+  if (plan->comm) return fail(S2_EINVAL, "communicator already initialised");
+  free_scratch(plan);
+  plan->world = world;
+  plan->rank = rank;
+  if (world > 1) {
+    ncclUniqueId id;
+    memcpy(&id, unique_id, sizeof id);
+    S2_NCCL(ncclCommInitRank(&plan->comm, world, id, rank), "ncclCommInitRank");
+  }
+  return ensure_scratch(plan);
+}
+
+int s2_comm_check(s2_plan* plan, void* stream) {
+  if (!plan) return fail(S2_EINVAL, "NULL plan");
+  if (plan->world == 1) return S2_OK;
+  const Plan& q = plan->p;
+  // compat_key digest: partition + sketch params (sparse.py:105-109)
+  const uint64_t parts[7] = {(uint64_t)q.dim, (uint64_t)q.num_blocks, (uint64_t)q.hp.rows,
+                             (uint64_t)q.hp.cols, q.seed, (uint64_t)q.injective, 0x53325348ull};
+  const uint64_t mine = derive(parts, 7);
+  uint64_t* d = nullptr;
+  S2_CUDA(cudaMalloc(&d, sizeof(uint64_t) * (plan->world + 1)), "cudaMalloc(check)");
+  cudaStream_t st = as_stream(stream);
+  int rc = S2_OK;
+  std::vector<uint64_t> all(plan->world);
+  if (cudaMemcpyAsync(d, &mine, sizeof mine, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      ncclAllGather(d, d + 1, 1, ncclUint64, plan->comm, st) != ncclSuccess ||
+      cudaMemcpyAsync(all.data(), d + 1, sizeof(uint64_t) * plan->world, cudaMemcpyDeviceToHost, st) !=
+          cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess) {
+    rc = fail(S2_ENCCL, "parameter agreement exchange failed");
+  } else {
+    for (int r = 0; r < plan->world; ++r)
+      if (all[r] != mine) {
+        rc = fail(S2_EINCOMPAT, "incompatible payloads: field 'sketch_params' differs (rank %d vs rank %d)",
+                  plan->rank, r);
+        break;
+      }
+  }
+  cudaFree(d);
+  return rc;
+}
+
+int s2_aggregate(s2_plan* plan, float* table, const uint32_t* bitmap, uint32_t* union_out, void* stream) {
+  if (!plan || !table || !bitmap || !union_out) return fail(S2_EINVAL, "NULL argument to s2_aggregate");
+  cudaStream_t st = as_stream(stream);
+  const Plan& q = plan->p;
+  if (plan->world == 1) {
+    if (union_out != bitmap)
+      S2_CUDA(cudaMemcpyAsync(union_out, bitmap, sizeof(uint32_t) * q.words, cudaMemcpyDeviceToDevice, st),
+              "copy bitmap");
+    return S2_OK;
+  }
+  int rc = ensure_scratch(plan);
+  if (rc) return rc;
+  const size_t cells = (size_t)q.hp.rows * q.hp.cols;
+  // sketch sum (sketch.py:213-216) and bitmap gather, one NCCL group over NVLink
+  S2_NCCL(ncclGroupStart(), "ncclGroupStart");
+  S2_NCCL(ncclAllReduce(table, table, cells, ncclFloat32, ncclSum, plan->comm, st), "ncclAllReduce(table)");
+  S2_NCCL(ncclAllGather(bitmap, plan->gather, (size_t)q.words, ncclUint32, plan->comm, st),
+          "ncclAllGather(bitmap)");
+  S2_NCCL(ncclGroupEnd(), "ncclGroupEnd");
+  // BlockMask.union (sparse.py:55-58) — NCCL has no bitwise-OR reduction
+  S2_CUDA(s2::launch_bitmap_or(q.words, plan->gather, plan->world, union_out, st), "bitmap OR");
+  return S2_OK;
+}
+
+int s2_reduce(s2_plan* plan, const float* g, float* out, uint64_t* counters, void* stream) {
+  if (!plan || !g || !out) return fail(S2_EINVAL, "NULL argument to s2_reduce");
+  int rc = ensure_scratch(plan);
+  if (rc) return rc;
+  unsigned long long* cnt = counters ? reinterpret_cast<unsigned long long*>(counters) : plan->counters;
+  rc = s2_compress(plan, g, plan->bitmap, plan->table, S2_MASK_NONZERO, reinterpret_cast<uint64_t*>(cnt),
+                   stream);
+  if (rc) return rc;
+  const uint32_t* un = plan->bitmap;
+  if (plan->world > 1) {
+    rc = s2_aggregate(plan, plan->table, plan->bitmap, plan->unionmap, stream);
+    if (rc) return rc;
+    un = plan->unionmap;
+  }
+  return s2_decode(plan, un, plan->table, plan->world, out, stream);
+}
+
+}  // extern "C"

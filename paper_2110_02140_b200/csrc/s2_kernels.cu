@@ -1,0 +1,677 @@
+// s2_kernels.cu — sm_100a kernels of the S2 sparse-sketch reduce.
+//
+//   K1+K2  k_compress_elem / k_compress_blocks
+//          read g once (128-bit streaming loads), __ballot_sync bitmap words,
+//          warp-level prefix compaction of the non-zeros into a per-warp shared
+//          queue, and count-sketch insertion (r hashes, red.global.add.f32 into
+//          the L2-resident table) once 32 entries are queued, so every lane of
+//          the hashing warp is busy.  Replaces sparse_compress (sparse.py:151-171)
+//          + CountSketchTable.insert (sketch.py:102-112).
+//   K3b    k_bitmap_or — BlockMask.union over W gathered bitmaps (sparse.py:55-58)
+//   K4     k_decode — walk the union bitmap, compact set positions per warp tile,
+//          r gathers + lower-median network, ÷W (IEEE), dense float4 streaming
+//          stores incl. zeros.  Replaces sparse_decompress (sparse.py:199-214)
+//          + CountSketchTable.query (sketch.py:114-128).
+//   aux    k_compact_* (ordered (idx,val) compaction = selected_indices,
+//          sparse.py:44-49 / :164-168), k_selected_count (sparse.py:51-53),
+//          k_table_sum (sketch.py:213-216).
+//
+// Data layout: g float32[dim]; bitmap uint32[ceil(num_blocks/32)] LE bit order;
+// table float32[rows][cols] row-major.  A warp tile is 1024 elements = 32
+// bitmap words = 8 float4 per lane.
+#include <cstdio>
+
+#include "s2_common.cuh"
+#include "s2_kernels.h"
+
+namespace s2 {
+
+constexpr int kWarps = 8;
+constexpr int kThreads = kWarps * 32;
+constexpr int kTile = 1024;
+constexpr int kQCap = 32 + 128;
+
+static int g_num_sms = 0;
+static int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+// ------------------------------------------------------------------ insert
+
+template <int R>
+__device__ __forceinline__ void insert_one(uint64_t i, float v, float* __restrict__ table,
+                                           const HashParams& hp) {
+  const size_t cols = hp.cols;
+  if (hp.mode == kInjective) {
+    // injective mapping: bucket(i) = i, sign = +1 (core.py:131-141)
+#pragma unroll
+    for (int j = 0; j < (R > 0 ? R : S2_MAX_ROWS); ++j) {
+      if (R == 0 && j >= hp.rows) break;
+      atomicAdd(table + j * cols + i, v);
+    }
+    return;
+  }
+  const uint64_t x = index_term(i);
+#pragma unroll
+  for (int j = 0; j < (R > 0 ? R : S2_MAX_ROWS); ++j) {
+    if (R == 0 && j >= hp.rows) break;
+    const uint64_t w = mix64(hp.seed[j] + x);
+    const uint32_t b = bucket_of(w, hp);
+    atomicAdd(table + j * cols + b, (w >> 63) ? -v : v);  // RED.E.ADD.F32 (result unused)
+  }
+}
+
+// ------------------------------------------------------- compress (K1+K2)
+//
+// MODE 0: element bitmap (block size 1), mask = g != 0, bitmap written directly.
+// MODE 1: block bitmap built from g != 0 (block size > 1), atomicOr into a zeroed bitmap.
+// MODE 2: given block bitmap (any block size): insert non-zeros of set blocks only.
+template <int R, int MODE>
+__global__ void __launch_bounds__(kThreads)
+k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __restrict__ bitmap,
+           float* __restrict__ table, unsigned long long* __restrict__ counters,
+           const __grid_constant__ HashParams hp) {
+  __shared__ uint32_t s_qi[kWarps][kQCap];
+  __shared__ float s_qv[kWarps][kQCap];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  uint32_t* qi = s_qi[wib];
+  float* qv = s_qv[wib];
+  const int64_t ntiles = (dim + kTile - 1) / kTile;
+  const int64_t nelem_words = (dim + 31) / 32;
+  const int64_t nw = (int64_t)gridDim.x * kWarps;
+  const uint32_t lt = lanemask_lt();
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+
+  int qn = 0;                    // warp-uniform queue depth
+  unsigned long long nnz = 0;    // warp-uniform
+  unsigned long long sel = 0;    // per-lane selected coordinates (MODE 2)
+  uint32_t bad = 0;
+
+  for (int64_t t = (int64_t)blockIdx.x * kWarps + wib; t < ntiles; t += nw) {
+    const int64_t base = t * kTile;
+    float4 v[8];
+    if (base + kTile <= dim) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = __ldcs(g4 + (base >> 2) + k * 32 + lane);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int64_t e = base + k * 128 + lane * 4;
+        v[k].x = e + 0 < dim ? g[e + 0] : 0.f;
+        v[k].y = e + 1 < dim ? g[e + 1] : 0.f;
+        v[k].z = e + 2 < dim ? g[e + 2] : 0.f;
+        v[k].w = e + 3 < dim ? g[e + 3] : 0.f;
+      }
+    }
+    uint32_t mword = 0xFFFFFFFFu;  // element-level selection word of elements base+32*lane..
+    if (MODE == 2) {
+      mword = bs == 1 ? ((t * 32 + lane) < nelem_words ? __ldg(bitmap + t * 32 + lane) : 0u)
+                      : expand_blocks(bitmap, base + 32 * lane, dim, bs);
+      const int64_t e0 = base + 32 * lane;
+      if (e0 + 32 > dim) mword &= e0 >= dim ? 0u : range_mask(0, (int)(dim - e0));
+      sel += __popc(mword);
+    }
+    uint32_t myword = 0;  // non-zero word for elements base+32*lane..+31
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float4 x = v[k];
+      bad |= nonfinite(x.x) | nonfinite(x.y) | nonfinite(x.z) | nonfinite(x.w);
+      // -0.0 compares equal to 0 and is not a non-zero (sparse.py:167)
+      uint32_t nib = (uint32_t)(x.x != 0.f) | ((uint32_t)(x.y != 0.f) << 1) |
+                     ((uint32_t)(x.z != 0.f) << 2) | ((uint32_t)(x.w != 0.f) << 3);
+      if (MODE == 2) {
+        const uint32_t mk = __shfl_sync(kFull, mword, 4 * k + (lane >> 3));
+        nib &= (mk >> ((lane & 7) * 4)) & 0xFu;
+      }
+      if (__any_sync(kFull, nib)) {
+        // bitmap word 4k + (lane>>3): OR the 8 nibbles of each 8-lane group
+        uint32_t tw = nib << ((lane & 7) * 4);
+        tw |= __shfl_xor_sync(kFull, tw, 1);
+        tw |= __shfl_xor_sync(kFull, tw, 2);
+        tw |= __shfl_xor_sync(kFull, tw, 4);
+        const uint32_t wv = __shfl_sync(kFull, tw, (lane & 3) << 3);
+        if ((lane >> 2) == k) myword = wv;
+        // warp compaction of the non-zeros into the queue
+        const uint32_t b0 = __ballot_sync(kFull, nib & 1u);
+        const uint32_t b1 = __ballot_sync(kFull, nib & 2u);
+        const uint32_t b2 = __ballot_sync(kFull, nib & 4u);
+        const uint32_t b3 = __ballot_sync(kFull, nib & 8u);
+        int pos = qn + __popc(b0 & lt) + __popc(b1 & lt) + __popc(b2 & lt) + __popc(b3 & lt);
+        const int tot = __popc(b0) + __popc(b1) + __popc(b2) + __popc(b3);
+        const uint32_t e0 = (uint32_t)(base + k * 128 + lane * 4);
+        if (nib & 1u) { qi[pos] = e0 + 0; qv[pos] = x.x; ++pos; }
+        if (nib & 2u) { qi[pos] = e0 + 1; qv[pos] = x.y; ++pos; }
+        if (nib & 4u) { qi[pos] = e0 + 2; qv[pos] = x.z; ++pos; }
+        if (nib & 8u) { qi[pos] = e0 + 3; qv[pos] = x.w; ++pos; }
+        qn += tot;
+        nnz += (unsigned)tot;
+        __syncwarp();
+        while (qn >= 32) {
+          qn -= 32;
+          insert_one<R>(qi[qn + lane], qv[qn + lane], table, hp);
+        }
+        __syncwarp();
+      }
+    }
+    if (MODE == 0) {
+      const int64_t wi = t * 32 + lane;
+      if (wi < nelem_words) bitmap[wi] = myword;
+    } else if (MODE == 1) {
+      if (myword) {  // OR the flags of every block this 32-element span touches
+        const int64_t e0 = base + 32 * lane;
+        const int64_t e_end = e0 + 32 < dim ? e0 + 32 : dim;
+        int64_t b = e0 / bs, s = e0;
+        while (s < e_end) {
+          int64_t be = (b + 1) * bs;
+          if (be > e_end) be = e_end;
+          if (myword & range_mask((int)(s - e0), (int)(be - e0)))
+            atomicOr(bitmap + (b >> 5), 1u << (b & 31));
+          s = be;
+          ++b;
+        }
+      }
+    }
+  }
+  __syncwarp();
+  if (lane < qn) insert_one<R>(qi[lane], qv[lane], table, hp);
+  bad = __any_sync(kFull, bad);
+  if (MODE == 2) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sel += __shfl_xor_sync(kFull, sel, o);
+  }
+  if (lane == 0) {
+    if (nnz) atomicAdd(counters + S2_CNT_NNZ, nnz);
+    if (MODE == 0 && nnz) atomicAdd(counters + S2_CNT_SELECTED, nnz);
+    if (MODE == 2 && sel) atomicAdd(counters + S2_CNT_SELECTED, sel);
+    if (bad) atomicOr(counters + S2_CNT_NONFINITE, 1ull);
+  }
+}
+
+// ---------------------------------------------------------------- decode (K4)
+
+// lower median (element (R-1)/2 of the sorted estimates, sketch.py:127-128)
+template <int R>
+__device__ __forceinline__ float lower_median(float (&e)[R]) {
+  if constexpr (R == 1) {
+    return e[0];
+  } else if constexpr (R == 2) {
+    return fminf(e[0], e[1]);
+  } else if constexpr (R == 3) {
+    return fmaxf(fminf(e[0], e[1]), fminf(fmaxf(e[0], e[1]), e[2]));
+  } else {
+    // odd-even transposition sort network, fully unrolled in registers
+#pragma unroll
+    for (int p = 0; p < R; ++p) {
+#pragma unroll
+      for (int a = (p & 1); a + 1 < R; a += 2) {
+        const float lo = fminf(e[a], e[a + 1]);
+        const float hi = fmaxf(e[a], e[a + 1]);
+        e[a] = lo;
+        e[a + 1] = hi;
+      }
+    }
+    return e[(R - 1) / 2];
+  }
+}
+
+template <int R>
+__device__ __forceinline__ float query_one(uint64_t i, const float* __restrict__ table,
+                                           const HashParams& hp) {
+  const size_t cols = hp.cols;
+  float e[R];
+  if (hp.mode == kInjective) {
+#pragma unroll
+    for (int j = 0; j < R; ++j) e[j] = __ldg(table + j * cols + i);
+  } else {
+    const uint64_t x = index_term(i);
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const uint64_t w = mix64(hp.seed[j] + x);
+      const float t = __ldg(table + j * cols + bucket_of(w, hp));
+      e[j] = (w >> 63) ? -t : t;
+    }
+  }
+  return lower_median<R>(e);
+}
+
+template <int R, bool BLOCKS>
+__global__ void __launch_bounds__(kThreads)
+k_decode(const uint32_t* __restrict__ bitmap, int64_t dim, int64_t bs,
+         const float* __restrict__ table, float workers, float* __restrict__ out,
+         const __grid_constant__ HashParams hp) {
+  __shared__ uint16_t s_q[kWarps][kTile];
+  __shared__ __align__(16) float s_v[kWarps][kTile];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  uint16_t* q = s_q[wib];
+  float* vals = s_v[wib];
+  const int64_t ntiles = (dim + kTile - 1) / kTile;
+  const int64_t nelem_words = (dim + 31) / 32;
+  const int64_t nw = (int64_t)gridDim.x * kWarps;
+
+  for (int64_t t = (int64_t)blockIdx.x * kWarps + wib; t < ntiles; t += nw) {
+    const int64_t base = t * kTile;
+    const int64_t e0 = base + 32 * lane;
+    uint32_t word;
+    if (!BLOCKS) {
+      word = (t * 32 + lane) < nelem_words ? __ldg(bitmap + t * 32 + lane) : 0u;
+    } else {
+      word = expand_blocks(bitmap, e0, dim, bs);
+    }
+    if (e0 + 32 > dim) word &= e0 >= dim ? 0u : range_mask(0, (int)(dim - e0));
+    // warp exclusive scan of the per-lane set counts -> queue of set positions
+    const int cnt = __popc(word);
+    int pre = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(kFull, pre, o);
+      if (lane >= o) pre += n;
+    }
+    const int total = __shfl_sync(kFull, pre, 31);
+    pre -= cnt;
+    for (uint32_t w = word; w; w &= w - 1u) q[pre++] = (uint16_t)(lane * 32 + (__ffs(w) - 1));
+    __syncwarp();
+    for (int s = lane; s < total; s += 32) {
+      const int pos = q[s];
+      // IEEE division: sparse.py:213 divides the float64 query by workers
+      vals[pos] = __fdiv_rn(query_one<R>((uint64_t)(base + pos), table, hp), workers);
+    }
+    __syncwarp();
+    const bool full = base + kTile <= dim;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t wk = __shfl_sync(kFull, word, 4 * k + (lane >> 3));
+      const uint32_t nib = (wk >> ((lane & 7) * 4)) & 0xFu;
+      float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (nib) {
+        const float4 sv = *reinterpret_cast<const float4*>(vals + k * 128 + lane * 4);
+        o.x = (nib & 1u) ? sv.x : 0.f;
+        o.y = (nib & 2u) ? sv.y : 0.f;
+        o.z = (nib & 4u) ? sv.z : 0.f;
+        o.w = (nib & 8u) ? sv.w : 0.f;
+      }
+      const int64_t e = base + k * 128 + lane * 4;
+      if (full) {
+        __stcs(reinterpret_cast<float4*>(out + e), o);
+      } else {
+        if (e + 0 < dim) out[e + 0] = o.x;
+        if (e + 1 < dim) out[e + 1] = o.y;
+        if (e + 2 < dim) out[e + 2] = o.z;
+        if (e + 3 < dim) out[e + 3] = o.w;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ----------------------------------------------------------- bitmap OR (K3b)
+
+__global__ void k_bitmap_or(const uint32_t* __restrict__ stacked, int64_t words, int nmasks,
+                            uint32_t* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if ((words & 3) == 0 && (((uintptr_t)stacked | (uintptr_t)out) & 15) == 0) {
+    const int64_t w4 = words >> 2;
+    const uint4* s4 = reinterpret_cast<const uint4*>(stacked);
+    for (int64_t i = i0; i < w4; i += stride) {
+      uint4 a = __ldcs(s4 + i);
+      for (int m = 1; m < nmasks; ++m) {
+        const uint4 b = __ldcs(s4 + (int64_t)m * w4 + i);
+        a.x |= b.x; a.y |= b.y; a.z |= b.z; a.w |= b.w;
+      }
+      reinterpret_cast<uint4*>(out)[i] = a;
+    }
+  } else {
+    for (int64_t i = i0; i < words; i += stride) {
+      uint32_t a = stacked[i];
+      for (int m = 1; m < nmasks; ++m) a |= stacked[(int64_t)m * words + i];
+      out[i] = a;
+    }
+  }
+}
+
+// -------------------------------------------------------- table sum (merge)
+
+__global__ void k_table_sum(const float* __restrict__ stacked, int64_t cells, int ntables,
+                            float* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cells; i += stride) {
+    float a = stacked[i];
+    for (int m = 1; m < ntables; ++m) a += stacked[(int64_t)m * cells + i];  // left fold
+    out[i] = a;
+  }
+}
+
+// ----------------------------------------- selected coordinates (alpha * dim)
+
+__global__ void k_selected_count(const uint32_t* __restrict__ bitmap, int64_t num_blocks,
+                                 int64_t dim, int64_t bs, unsigned long long* __restrict__ counters) {
+  const int64_t words = (num_blocks + 31) / 32;
+  unsigned long long acc = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += stride) {
+    uint32_t bits = bitmap[w];
+    const int64_t b0 = w * 32;
+    if (b0 + 32 > num_blocks) bits &= range_mask(0, (int)(num_blocks - b0));
+    if ((b0 + 32) * bs <= dim) {
+      acc += (unsigned long long)__popc(bits) * (unsigned long long)bs;
+    } else {
+      for (; bits; bits &= bits - 1u) {  // ragged / empty tail blocks (core.py:202-206)
+        const int64_t b = b0 + __ffs(bits) - 1;
+        int64_t st = b * bs, en = st + bs;
+        if (st > dim) st = dim;
+        if (en > dim) en = dim;
+        acc += (unsigned long long)(en - st);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(counters + S2_CNT_SELECTED, acc);
+}
+
+// ------------------------------------------------- ordered compaction (aux)
+//
+// Three passes over 1024-element tiles: count, exclusive scan, write.  The
+// element word of lane L covers elements base+32L..+31; with g != NULL it is
+// ANDed with the non-zero bits of g (sparse.py:164-168).
+
+__device__ __forceinline__ uint32_t compact_word(const uint32_t* __restrict__ bitmap,
+                                                 const float* __restrict__ g, int64_t dim,
+                                                 int64_t bs, int64_t e0, float (&vals)[32]) {
+  uint32_t word;
+  if (bs == 1) {
+    word = e0 < dim ? __ldg(bitmap + (e0 >> 5)) : 0u;
+  } else {
+    word = expand_blocks(bitmap, e0, dim, bs);
+  }
+  if (e0 + 32 > dim) word &= e0 >= dim ? 0u : range_mask(0, (int)(dim - e0));
+  if (g != nullptr && word) {
+    uint32_t nzw = 0;
+    if (e0 + 32 <= dim) {
+      const float4* p = reinterpret_cast<const float4*>(g + e0);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float4 x = __ldg(p + k);
+        vals[4 * k + 0] = x.x; vals[4 * k + 1] = x.y; vals[4 * k + 2] = x.z; vals[4 * k + 3] = x.w;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 32; ++k) vals[k] = e0 + k < dim ? g[e0 + k] : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < 32; ++k) nzw |= (uint32_t)(vals[k] != 0.f) << k;
+    word &= nzw;
+  }
+  return word;
+}
+
+__global__ void __launch_bounds__(kThreads)
+k_compact_count(const uint32_t* __restrict__ bitmap, const float* __restrict__ g, int64_t dim,
+                int64_t bs, int64_t* __restrict__ tile_counts) {
+  const int lane = threadIdx.x & 31;
+  const int64_t ntiles = (dim + kTile - 1) / kTile;
+  const int64_t nw = (int64_t)gridDim.x * kWarps;
+  for (int64_t t = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); t < ntiles; t += nw) {
+    float vals[32];
+    const uint32_t word = compact_word(bitmap, g, dim, bs, t * kTile + 32 * lane, vals);
+    int c = __popc(word);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+    if (lane == 0) tile_counts[t] = c;
+  }
+}
+
+// single-CTA exclusive scan of n int64 counts (in place); total into *total
+__global__ void __launch_bounds__(1024) k_scan(int64_t* __restrict__ a, int64_t n,
+                                               int64_t* __restrict__ total) {
+  __shared__ int64_t s_warp[32];
+  const int tid = threadIdx.x;
+  const int64_t per = (n + blockDim.x - 1) / blockDim.x;
+  const int64_t lo = tid * per;
+  const int64_t hi = lo + per < n ? lo + per : n;
+  int64_t sum = 0;
+  for (int64_t i = lo; i < hi; ++i) sum += a[i];
+  // block exclusive scan of sum
+  const int lane = tid & 31, wid = tid >> 5;
+  int64_t inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t v = __shfl_up_sync(kFull, inc, o);
+    if (lane >= o) inc += v;
+  }
+  if (lane == 31) s_warp[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    int64_t ws = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0;
+    int64_t wi = ws;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t v = __shfl_up_sync(kFull, wi, o);
+      if (lane >= o) wi += v;
+    }
+    s_warp[lane] = wi - ws;
+    if (lane == 31) *total = wi;
+  }
+  __syncthreads();
+  int64_t run = s_warp[wid] + inc - sum;
+  for (int64_t i = lo; i < hi; ++i) {
+    const int64_t c = a[i];
+    a[i] = run;
+    run += c;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+k_compact_write(const uint32_t* __restrict__ bitmap, const float* __restrict__ g, int64_t dim,
+                int64_t bs, const int64_t* __restrict__ tile_offsets, int64_t* __restrict__ idx_out,
+                float* __restrict__ val_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t ntiles = (dim + kTile - 1) / kTile;
+  const int64_t nw = (int64_t)gridDim.x * kWarps;
+  for (int64_t t = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); t < ntiles; t += nw) {
+    float vals[32];
+    const int64_t e0 = t * kTile + 32 * lane;
+    uint32_t word = compact_word(bitmap, g, dim, bs, e0, vals);
+    const int cnt = __popc(word);
+    int pre = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(kFull, pre, o);
+      if (lane >= o) pre += n;
+    }
+    int64_t pos = tile_offsets[t] + pre - cnt;
+    for (; word; word &= word - 1u) {
+      const int b = __ffs(word) - 1;
+      idx_out[pos] = e0 + b;
+      if (val_out != nullptr) {
+#pragma unroll
+        for (int k = 0; k < 32; ++k)
+          if (k == b) val_out[pos] = vals[k];
+      }
+      ++pos;
+    }
+  }
+}
+
+// ------------------------------------- CountSketchTable.insert / .query (pairs)
+
+template <int R>
+__global__ void k_insert_pairs(const int64_t* __restrict__ idx, const float* __restrict__ vals, int64_t n,
+                               float* __restrict__ table, const __grid_constant__ HashParams hp) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+    const float v = vals[k];
+    if (v != 0.f) insert_one<R>((uint64_t)idx[k], v, table, hp);  // zero values are no-ops (sketch.py:103)
+  }
+}
+
+template <int R>
+__global__ void k_query_pairs(const int64_t* __restrict__ idx, int64_t n, const float* __restrict__ table,
+                              float* __restrict__ out, const __grid_constant__ HashParams hp) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride)
+    out[k] = query_one<R>((uint64_t)idx[k], table, hp);
+}
+
+// =================================================================== launchers
+
+static int grid_for(int64_t ntiles, int ctas_per_sm) {
+  const int64_t want = (ntiles + kWarps - 1) / kWarps;
+  const int64_t cap = (int64_t)num_sms() * ctas_per_sm;
+  int64_t gr = want < cap ? want : cap;
+  return gr < 1 ? 1 : (int)gr;
+}
+
+template <int R>
+static void launch_compress_r(const Plan& p, const float* g, uint32_t* bitmap, float* table,
+                              unsigned long long* counters, int mode, cudaStream_t st) {
+  const int64_t ntiles = (p.dim + kTile - 1) / kTile;
+  const int grid = grid_for(ntiles, 4);
+  if (mode == S2_MASK_GIVEN) {
+    k_compress<R, 2><<<grid, kThreads, 0, st>>>(g, p.dim, p.block_size, bitmap, table, counters, p.hp);
+  } else if (p.block_size == 1) {
+    k_compress<R, 0><<<grid, kThreads, 0, st>>>(g, p.dim, p.block_size, bitmap, table, counters, p.hp);
+  } else {
+    k_compress<R, 1><<<grid, kThreads, 0, st>>>(g, p.dim, p.block_size, bitmap, table, counters, p.hp);
+  }
+}
+
+cudaError_t launch_compress(const Plan& p, const float* g, uint32_t* bitmap, float* table,
+                            unsigned long long* counters, int mode, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(table, 0, sizeof(float) * (size_t)p.hp.rows * p.hp.cols, st);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(counters, 0, sizeof(unsigned long long) * S2_NUM_COUNTERS, st);
+  if (e != cudaSuccess) return e;
+  if (mode == S2_MASK_NONZERO && p.block_size > 1) {
+    e = cudaMemsetAsync(bitmap, 0, sizeof(uint32_t) * (size_t)p.words, st);
+    if (e != cudaSuccess) return e;
+  }
+  switch (p.hp.rows) {
+    case 1: launch_compress_r<1>(p, g, bitmap, table, counters, mode, st); break;
+    case 3: launch_compress_r<3>(p, g, bitmap, table, counters, mode, st); break;
+    case 5: launch_compress_r<5>(p, g, bitmap, table, counters, mode, st); break;
+    default: launch_compress_r<0>(p, g, bitmap, table, counters, mode, st); break;
+  }
+  if (mode == S2_MASK_NONZERO && p.block_size > 1) {
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return launch_selected_count(p, bitmap, counters, st);
+  }
+  return cudaGetLastError();
+}
+
+template <int R>
+static void launch_decode_r(const Plan& p, const uint32_t* bitmap, const float* table, int workers,
+                            float* out, cudaStream_t st) {
+  const int64_t ntiles = (p.dim + kTile - 1) / kTile;
+  const int grid = grid_for(ntiles, 4);
+  if (p.block_size == 1)
+    k_decode<R, false><<<grid, kThreads, 0, st>>>(bitmap, p.dim, 1, table, (float)workers, out, p.hp);
+  else
+    k_decode<R, true><<<grid, kThreads, 0, st>>>(bitmap, p.dim, p.block_size, table, (float)workers, out, p.hp);
+}
+
+cudaError_t launch_decode(const Plan& p, const uint32_t* bitmap, const float* table, int workers,
+                          float* out, cudaStream_t st) {
+  switch (p.hp.rows) {
+    case 1: launch_decode_r<1>(p, bitmap, table, workers, out, st); break;
+    case 2: launch_decode_r<2>(p, bitmap, table, workers, out, st); break;
+    case 3: launch_decode_r<3>(p, bitmap, table, workers, out, st); break;
+    case 4: launch_decode_r<4>(p, bitmap, table, workers, out, st); break;
+    case 5: launch_decode_r<5>(p, bitmap, table, workers, out, st); break;
+    case 6: launch_decode_r<6>(p, bitmap, table, workers, out, st); break;
+    case 7: launch_decode_r<7>(p, bitmap, table, workers, out, st); break;
+    case 8: launch_decode_r<8>(p, bitmap, table, workers, out, st); break;
+    case 9: launch_decode_r<9>(p, bitmap, table, workers, out, st); break;
+    case 10: launch_decode_r<10>(p, bitmap, table, workers, out, st); break;
+    case 11: launch_decode_r<11>(p, bitmap, table, workers, out, st); break;
+    case 12: launch_decode_r<12>(p, bitmap, table, workers, out, st); break;
+    case 13: launch_decode_r<13>(p, bitmap, table, workers, out, st); break;
+    case 14: launch_decode_r<14>(p, bitmap, table, workers, out, st); break;
+    case 15: launch_decode_r<15>(p, bitmap, table, workers, out, st); break;
+    case 16: launch_decode_r<16>(p, bitmap, table, workers, out, st); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bitmap_or(int64_t words, const uint32_t* stacked, int nmasks, uint32_t* out,
+                             cudaStream_t st) {
+  if (words <= 0) return cudaSuccess;
+  const int64_t n = (words & 3) == 0 ? words / 4 : words;
+  int64_t grid = (n + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  if (grid > cap) grid = cap;
+  k_bitmap_or<<<(int)grid, 256, 0, st>>>(stacked, words, nmasks, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_table_sum(int64_t cells, const float* stacked, int ntables, float* out,
+                             cudaStream_t st) {
+  if (cells <= 0) return cudaSuccess;
+  int64_t grid = (cells + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  if (grid > cap) grid = cap;
+  k_table_sum<<<(int)grid, 256, 0, st>>>(stacked, cells, ntables, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_selected_count(const Plan& p, const uint32_t* bitmap,
+                                  unsigned long long* counters, cudaStream_t st) {
+  int64_t grid = (p.words + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  if (grid > cap) grid = cap;
+  if (grid < 1) grid = 1;
+  k_selected_count<<<(int)grid, 256, 0, st>>>(bitmap, p.num_blocks, p.dim, p.block_size, counters);
+  return cudaGetLastError();
+}
+
+int64_t compact_scratch_bytes(const Plan& p) {
+  const int64_t ntiles = (p.dim + kTile - 1) / kTile;
+  return (ntiles + 1) * (int64_t)sizeof(int64_t);
+}
+
+cudaError_t launch_compact(const Plan& p, const uint32_t* bitmap, const float* g, int64_t* idx_out,
+                           float* val_out, int64_t* count, void* scratch, cudaStream_t st) {
+  const int64_t ntiles = (p.dim + kTile - 1) / kTile;
+  int64_t* tiles = reinterpret_cast<int64_t*>(scratch);
+  const int grid = grid_for(ntiles, 4);
+  k_compact_count<<<grid, kThreads, 0, st>>>(bitmap, g, p.dim, p.block_size, tiles);
+  k_scan<<<1, 1024, 0, st>>>(tiles, ntiles, count);
+  k_compact_write<<<grid, kThreads, 0, st>>>(bitmap, g, p.dim, p.block_size, tiles, idx_out, val_out);
+  return cudaGetLastError();
+}
+
+template <int R>
+static void launch_pairs_r(const Plan& p, const int64_t* idx, const float* vals, int64_t n, float* table,
+                           float* out, cudaStream_t st) {
+  int64_t grid = (n + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  if (grid > cap) grid = cap;
+  if (vals) k_insert_pairs<R><<<(int)grid, 256, 0, st>>>(idx, vals, n, table, p.hp);
+  else k_query_pairs<R><<<(int)grid, 256, 0, st>>>(idx, n, table, out, p.hp);
+}
+
+cudaError_t launch_pairs(const Plan& p, const int64_t* idx, const float* vals, int64_t n, const float* table_in,
+                         float* out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  float* table = const_cast<float*>(table_in);
+  switch (p.hp.rows) {
+#define S2_CASE(r) case r: launch_pairs_r<r>(p, idx, vals, n, table, out, st); break;
+    S2_CASE(1) S2_CASE(2) S2_CASE(3) S2_CASE(4) S2_CASE(5) S2_CASE(6) S2_CASE(7) S2_CASE(8)
+    S2_CASE(9) S2_CASE(10) S2_CASE(11) S2_CASE(12) S2_CASE(13) S2_CASE(14) S2_CASE(15) S2_CASE(16)
+#undef S2_CASE
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace s2

@@ -1,0 +1,40 @@
+// s2_kernels.h — internal launcher interface between the C ABI (s2_capi.cu) and the kernels.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "s2_common.cuh"
+
+namespace s2 {
+
+// BlockPartition(dim, num_blocks) + CountSketchTable hash parameters (core.py:172-211, sketch.py:86-100)
+struct Plan {
+  int64_t dim;
+  int64_t num_blocks;
+  int64_t block_size;  // ceil(dim / num_blocks)
+  int64_t words;       // ceil(num_blocks / 32)
+  uint64_t seed;
+  int injective;
+  HashParams hp;
+};
+
+cudaError_t launch_compress(const Plan& p, const float* g, uint32_t* bitmap, float* table,
+                            unsigned long long* counters, int mode, cudaStream_t st);
+cudaError_t launch_decode(const Plan& p, const uint32_t* bitmap, const float* table, int workers,
+                          float* out, cudaStream_t st);
+cudaError_t launch_bitmap_or(int64_t words, const uint32_t* stacked, int nmasks, uint32_t* out,
+                             cudaStream_t st);
+cudaError_t launch_table_sum(int64_t cells, const float* stacked, int ntables, float* out,
+                             cudaStream_t st);
+cudaError_t launch_selected_count(const Plan& p, const uint32_t* bitmap,
+                                  unsigned long long* counters, cudaStream_t st);
+int64_t compact_scratch_bytes(const Plan& p);
+cudaError_t launch_compact(const Plan& p, const uint32_t* bitmap, const float* g, int64_t* idx_out,
+                           float* val_out, int64_t* count, void* scratch, cudaStream_t st);
+
+// CountSketchTable.insert (vals != NULL) or .query (vals == NULL -> out) on explicit index lists
+cudaError_t launch_pairs(const Plan& p, const int64_t* idx, const float* vals, int64_t n, const float* table,
+                         float* out, cudaStream_t st);
+
+}  // namespace s2

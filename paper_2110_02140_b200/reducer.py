@@ -1,0 +1,83 @@
+"""Distributed S2 reduce: one process per GPU, NCCL over NVLink inside libs2.so.
+
+This replaces the reference's in-process ``sparse_merge`` list fold
+(sparse.py:174-196) with a real box-wide exchange:
+
+    compress (K1+K2, local)  ->  sketch all-reduce + bitmap all-gather/OR (K3)
+                             ->  decode (K4, replicated on every rank, ÷W)
+
+``S2Reducer.reduce(g)`` is one C call (``s2_reduce``) on the caller's CUDA
+stream; no host synchronisation happens inside it, so it can be captured in
+a CUDA graph.  The NCCL communicator is created once from a unique id that
+rank 0 broadcasts through torch.distributed (any backend).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from ._lib import S2_CNT_NNZ, S2_CNT_NONFINITE, S2_NUM_COUNTERS, check, lib, ptr, stream_ptr
+from .core import as_gradient
+from .sketch import Plan
+from .sparse import DEFAULT_ROWS, DEFAULT_SIZE_RATIO, sketch_cols
+
+
+class S2Reducer:
+    """Averaged sparse-sketch all-reduce of a flat float32 gradient.
+
+    Parameters mirror ``SparseSketchCompressor`` (sparse.py:294-305): ``cols``
+    defaults to ``sketch_cols(size_ratio, alpha, dim, rows)``; ``num_blocks``
+    defaults to ``dim`` (element bitmap, the north-star mask rule).
+    """
+
+    def __init__(self, dim: int, rows: int = DEFAULT_ROWS, cols: int | None = None, seed: int = 0,
+                 num_blocks: int | None = None, size_ratio: float = DEFAULT_SIZE_RATIO,
+                 alpha: float | None = None, group=None, world: int | None = None, rank: int | None = None):
+        import torch.distributed as dist
+
+        if cols is None:
+            if alpha is None:
+                raise ValueError("give cols, or alpha (expected non-zero fraction) to size the sketch")
+            cols = sketch_cols(size_ratio, alpha, dim, rows)
+        self.dim, self.rows, self.cols, self.seed = int(dim), int(rows), int(cols), int(seed)
+        self.num_blocks = int(num_blocks or dim)
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        self.plan = Plan(self.dim, self.num_blocks, self.rows, self.cols, self.seed)
+        if world is None:
+            world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+        if rank is None:
+            rank = dist.get_rank(group) if world > 1 else 0
+        self.world, self.rank = int(world), int(rank)
+        uid = (ctypes.c_uint8 * 128)()
+        if self.world > 1:
+            if self.rank == 0:
+                check(lib.s2_nccl_unique_id(uid), "nccl unique id")
+            box = [bytes(uid)]
+            dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                       group=group)
+            ctypes.memmove(uid, box[0], 128)
+        check(lib.s2_comm_init(self.plan.handle, self.world, self.rank, uid), "comm init")
+        check(lib.s2_comm_check(self.plan.handle, stream_ptr()), "comm check")
+        self.counters = torch.zeros(S2_NUM_COUNTERS, dtype=torch.int64, device=self.device)
+
+    def reduce(self, g: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """Averaged gradient estimate: median-of-rows sketch query ÷ world at every union-bitmap
+        coordinate, 0 elsewhere (sparse_decompress of sparse_merge of every rank's sparse_compress)."""
+        if g.numel() != self.dim:
+            raise ValueError(f"dimension mismatch: mask dim {self.dim}, vector {g.numel()}")
+        if not (g.is_cuda and g.dtype == torch.float32 and g.is_contiguous() and g.data_ptr() % 16 == 0):
+            g = as_gradient(g, self.device)
+        if out is None:
+            out = torch.empty(self.dim, dtype=torch.float32, device=self.device)
+        check(lib.s2_reduce(self.plan.handle, ptr(g), ptr(out), ptr(self.counters), stream_ptr(stream)), "reduce")
+        return out
+
+    def check_finite(self) -> None:
+        """Raise the reference's ValueError if the last reduced gradient held NaN/Inf (syncs)."""
+        if int(self.counters[S2_CNT_NONFINITE]):
+            raise ValueError("gradient vector contains NaN or Inf")
+
+    def last_nnz(self) -> int:
+        return int(self.counters[S2_CNT_NNZ])
