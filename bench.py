@@ -239,12 +239,12 @@ def ours(args, cfg):
     stream = torch.cuda.current_stream()
     sp = ctypes.c_void_p(stream.cuda_stream)
     h = red.plan.handle
-    cnt = ptr(red.counters)
     gp = [ptr(g) for g in grads]
     op = [ptr(x) for x in outs]
+    null = ctypes.c_void_p(0)
 
     def step(i):
-        check(lib.s2_reduce(h, gp[i % N_ROTATE], op[i % N_ROTATE], cnt, sp))
+        check(lib.s2_reduce(h, gp[i % N_ROTATE], op[i % N_ROTATE], null, sp))
 
     def barrier():
         torch.cuda.synchronize()
@@ -259,7 +259,7 @@ def ours(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    clocks = ClockSampler(local) if rank == 0 or True else None
+    clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.2)
     clocks.mark("load_start")
@@ -283,28 +283,23 @@ def ours(args, cfg):
     barrier()
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
 
-    # per-phase durations (same launches, events between them) for the roofline
-    counters = red.counters
-    tab = torch.empty(rows * cols, dtype=torch.float32, device="cuda")
-    bm = torch.empty(-(-d // 32) + 4, dtype=torch.int32, device="cuda")
-    un = torch.empty_like(bm)
-    phases = {"compress": 0.0, "aggregate": 0.0, "decode": 0.0}
+    # per-phase durations: the same s2_reduce launches with the plan's timing events
+    # (recorded on the launching stream between compress / aggregate / decode)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    for e in ev:
+        e.record(stream)
+    evs = (ctypes.c_void_p * 4)(*[e.cuda_event for e in ev])
+    check(lib.s2_plan_set_timing_events(h, evs, 4))
+    phases = {"compress": 0.0, "aggregate": 0.0, "decode": 0.0}
     nph = max(args.steps, 20)
     barrier()
     for i in range(nph):
-        ev[0].record(stream)
-        check(lib.s2_compress(h, gp[i % N_ROTATE], ptr(bm), ptr(tab), 0, cnt, sp))
-        ev[1].record(stream)
-        if world > 1:
-            check(lib.s2_aggregate(h, ptr(tab), ptr(bm), ptr(un), sp))
-        ev[2].record(stream)
-        check(lib.s2_decode(h, ptr(un) if world > 1 else ptr(bm), ptr(tab), world, op[i % N_ROTATE], sp))
-        ev[3].record(stream)
+        step(i)
         ev[3].synchronize()
         phases["compress"] += ev[0].elapsed_time(ev[1])
         phases["aggregate"] += ev[1].elapsed_time(ev[2])
         phases["decode"] += ev[2].elapsed_time(ev[3])
+    check(lib.s2_plan_set_timing_events(h, None, 0))
     phases = {k: max_over_ranks(v / nph) for k, v in phases.items()}
 
     # e2e: pinned host gradient in, pinned host result out, copies inside the timed region

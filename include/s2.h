@@ -128,8 +128,18 @@ int s2_comm_check(s2_plan* plan, void* stream);
 int s2_aggregate(s2_plan* plan, float* table, const uint32_t* bitmap, uint32_t* union_out,
                  void* stream);
 /* the whole reduce: compress -> aggregate -> decode (÷ world) using plan-owned
- * scratch; out = float32[dim] averaged gradient.  counters may be NULL. */
+ * scratch; out = float32[dim] averaged gradient.  counters may be NULL (then the
+ * plan's own are used, see s2_last_counters).  Plan-owned sketch tables and
+ * counters alternate between consecutive calls (the decode of call i zeroes the
+ * buffers of call i+1), so a CUDA graph must capture an even number of calls. */
 int s2_reduce(s2_plan* plan, const float* g, float* out, uint64_t* counters, void* stream);
+/* device pointer to the counters of the most recent s2_reduce(counters = NULL) */
+const uint64_t* s2_last_counters(const s2_plan* plan);
+/* optional: 4 caller-created cudaEvent_t that s2_reduce records before compress,
+ * after compress, after aggregate and after decode (n = 0 disables) */
+int s2_plan_set_timing_events(s2_plan* plan, void* const* events, int n);
+/* copy those counters to host (synchronises `stream`) */
+int s2_read_counters(const s2_plan* plan, uint64_t* host_out, void* stream);
 int s2_plan_world(const s2_plan* plan);
 
 #ifdef __cplusplus

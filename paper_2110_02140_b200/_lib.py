@@ -56,13 +56,16 @@ SIGNATURES = {
     "s2_aggregate": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "s2_reduce": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "s2_plan_world": (c_int, [c_void_p]),
+    "s2_last_counters": (c_void_p, [c_void_p]),
+    "s2_read_counters": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "s2_plan_set_timing_events": (c_int, [c_void_p, c_void_p, c_int]),
 }
 
 
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
-            f"{LIB_PATH} is missing: build it with `python -m paper_2110_02140_b200.build` "
+            f"{LIB_PATH} is missing: build it with `python paper_2110_02140_b200/build.py` "
             "(there is no CPU fallback for the S2 path)"
         )
     # make sure torch's libnccl/libcudart are loaded first so libs2.so binds to the same copies

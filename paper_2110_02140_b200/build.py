@@ -1,6 +1,6 @@
 """Build libs2.so in-tree with nvcc for sm_100a (no JIT cache: the .so travels with gpurun).
 
-    python -m paper_2110_02140_b200.build
+    python paper_2110_02140_b200/build.py [--force]
 """
 
 from __future__ import annotations

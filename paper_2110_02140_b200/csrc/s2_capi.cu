@@ -21,12 +21,16 @@ struct s2_plan {
   int world = 1;
   int rank = 0;
   ncclComm_t comm = nullptr;
-  // plan-owned scratch for s2_reduce / s2_aggregate
-  float* table = nullptr;
+  // plan-owned scratch for s2_reduce / s2_aggregate.  Sketch tables and counters
+  // ping-pong: the decode of reduce i zeroes the buffers reduce i+1 compresses into,
+  // so the hot path has no memset launches.
+  float* tables[2] = {nullptr, nullptr};
+  unsigned long long* counters[2] = {nullptr, nullptr};
+  int phase = 0;
   uint32_t* bitmap = nullptr;
   uint32_t* unionmap = nullptr;
   uint32_t* gather = nullptr;  // world * words (all-gather landing buffer)
-  unsigned long long* counters = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // optional phase timing events
 };
 
 namespace {
@@ -157,14 +161,16 @@ int s2_plan_create(int64_t dim, int64_t num_blocks, int rows, int64_t cols, uint
 }
 
 static void free_scratch(s2_plan* p) {
-  cudaFree(p->table);
+  for (int k = 0; k < 2; ++k) {
+    cudaFree(p->tables[k]);
+    cudaFree(p->counters[k]);
+    p->tables[k] = nullptr;
+    p->counters[k] = nullptr;
+  }
   cudaFree(p->bitmap);
   cudaFree(p->unionmap);
   cudaFree(p->gather);
-  cudaFree(p->counters);
-  p->table = nullptr;
   p->bitmap = p->unionmap = p->gather = nullptr;
-  p->counters = nullptr;
 }
 
 void s2_plan_destroy(s2_plan* plan) {
@@ -259,15 +265,21 @@ int s2_nccl_unique_id(void* out) {
 }
 
 static int ensure_scratch(s2_plan* p) {
-  if (p->table) return S2_OK;
-  const size_t cells = (size_t)p->p.hp.rows * p->p.hp.cols;
+  if (p->tables[0]) return S2_OK;
+  const size_t cells4 = ((size_t)p->p.hp.rows * p->p.hp.cols + 3) / 4 * 4;  // decode zeroes float4s
   const size_t wb = sizeof(uint32_t) * ((size_t)p->p.words + 4);
-  S2_CUDA(cudaMalloc(&p->table, cells * sizeof(float)), "cudaMalloc(table)");
+  for (int k = 0; k < 2; ++k) {
+    S2_CUDA(cudaMalloc(&p->tables[k], cells4 * sizeof(float)), "cudaMalloc(table)");
+    S2_CUDA(cudaMemset(p->tables[k], 0, cells4 * sizeof(float)), "cudaMemset(table)");
+    S2_CUDA(cudaMalloc(&p->counters[k], sizeof(unsigned long long) * S2_NUM_COUNTERS), "cudaMalloc(counters)");
+    S2_CUDA(cudaMemset(p->counters[k], 0, sizeof(unsigned long long) * S2_NUM_COUNTERS), "cudaMemset(counters)");
+  }
+  p->phase = 0;
   S2_CUDA(cudaMalloc(&p->bitmap, wb), "cudaMalloc(bitmap)");
   S2_CUDA(cudaMalloc(&p->unionmap, wb), "cudaMalloc(union)");
-  S2_CUDA(cudaMalloc(&p->counters, sizeof(unsigned long long) * S2_NUM_COUNTERS), "cudaMalloc(counters)");
   if (p->world > 1)
     S2_CUDA(cudaMalloc(&p->gather, sizeof(uint32_t) * (size_t)p->p.words * p->world), "cudaMalloc(gather)");
+  S2_CUDA(cudaDeviceSynchronize(), "scratch init");
   return S2_OK;
 }
 
@@ -343,19 +355,56 @@ int s2_aggregate(s2_plan* plan, float* table, const uint32_t* bitmap, uint32_t* 
 
 int s2_reduce(s2_plan* plan, const float* g, float* out, uint64_t* counters, void* stream) {
   if (!plan || !g || !out) return fail(S2_EINVAL, "NULL argument to s2_reduce");
+  if (reinterpret_cast<uintptr_t>(g) & 15) return fail(S2_EINVAL, "gradient must be 16-byte aligned");
+  if (reinterpret_cast<uintptr_t>(out) & 15) return fail(S2_EINVAL, "output must be 16-byte aligned");
   int rc = ensure_scratch(plan);
   if (rc) return rc;
-  unsigned long long* cnt = counters ? reinterpret_cast<unsigned long long*>(counters) : plan->counters;
-  rc = s2_compress(plan, g, plan->bitmap, plan->table, S2_MASK_NONZERO, reinterpret_cast<uint64_t*>(cnt),
-                   stream);
-  if (rc) return rc;
+  cudaStream_t st = as_stream(stream);
+  const int cur = plan->phase, nxt = cur ^ 1;
+  float* table = plan->tables[cur];
+  // caller counters: zeroed by memset; plan counters: zeroed by the previous decode
+  unsigned long long* cnt = counters ? reinterpret_cast<unsigned long long*>(counters) : plan->counters[cur];
+  if (plan->ev[0]) cudaEventRecord(plan->ev[0], st);
+  S2_CUDA(s2::launch_compress(plan->p, g, plan->bitmap, table, cnt, S2_MASK_NONZERO, st, counters == nullptr),
+          "s2_reduce/compress");
+  if (plan->ev[1]) cudaEventRecord(plan->ev[1], st);
   const uint32_t* un = plan->bitmap;
   if (plan->world > 1) {
-    rc = s2_aggregate(plan, plan->table, plan->bitmap, plan->unionmap, stream);
+    rc = s2_aggregate(plan, table, plan->bitmap, plan->unionmap, stream);
     if (rc) return rc;
     un = plan->unionmap;
   }
-  return s2_decode(plan, un, plan->table, plan->world, out, stream);
+  if (plan->ev[2]) cudaEventRecord(plan->ev[2], st);
+  S2_CUDA(s2::launch_decode(plan->p, un, table, plan->world, out, st, plan->tables[nxt], plan->counters[nxt]),
+          "s2_reduce/decode");
+  if (plan->ev[3]) cudaEventRecord(plan->ev[3], st);
+  plan->phase = nxt;
+  return S2_OK;
+}
+
+int s2_plan_set_timing_events(s2_plan* plan, void* const* events, int n) {
+  if (!plan) return fail(S2_EINVAL, "NULL plan");
+  if (n != 0 && n != 4) return fail(S2_EINVAL, "need 0 or 4 events");
+  for (int k = 0; k < 4; ++k) plan->ev[k] = n ? reinterpret_cast<cudaEvent_t>(events[k]) : nullptr;
+  return S2_OK;
+}
+
+int s2_read_counters(const s2_plan* plan, uint64_t* host_out, void* stream) {
+  if (!plan || !host_out) return fail(S2_EINVAL, "NULL argument to s2_read_counters");
+  if (!plan->counters[0]) {
+    memset(host_out, 0, sizeof(uint64_t) * S2_NUM_COUNTERS);
+    return S2_OK;
+  }
+  cudaStream_t st = as_stream(stream);
+  S2_CUDA(cudaMemcpyAsync(host_out, plan->counters[plan->phase ^ 1], sizeof(uint64_t) * S2_NUM_COUNTERS,
+                          cudaMemcpyDeviceToHost, st), "read counters");
+  S2_CUDA(cudaStreamSynchronize(st), "read counters");
+  return S2_OK;
+}
+
+const uint64_t* s2_last_counters(const s2_plan* plan) {
+  if (!plan || !plan->counters[0]) return nullptr;
+  return reinterpret_cast<const uint64_t*>(plan->counters[plan->phase ^ 1]);
 }
 
 }  // extern "C"

@@ -72,13 +72,38 @@ __device__ __forceinline__ void insert_one(uint64_t i, float v, float* __restric
 // MODE 0: element bitmap (block size 1), mask = g != 0, bitmap written directly.
 // MODE 1: block bitmap built from g != 0 (block size > 1), atomicOr into a zeroed bitmap.
 // MODE 2: given block bitmap (any block size): insert non-zeros of set blocks only.
+//
+// Per warp tile (1024 elements): lane l holds float4 chunks k = 0..7 at elements
+// base + 128k + 4l (coalesced 512 B per load instruction).  Its 32 non-zero flags
+// form one register m (bit 4k+c <-> element base+128k+4l+c).  The bitmap word of
+// lane L (elements base+32L..+31) is the transpose of m across the 8-lane group
+// (8 shuffles).  Non-zeros are appended to a per-warp shared queue at positions
+// from one warp scan of popc(m); every full batch of 32 is hashed and inserted by
+// the 32 lanes together.  NaN/Inf are non-zeros, so finiteness is tested on the
+// queue only (MODE 2 tests every element: unselected non-zeros never reach the queue).
+constexpr int kQFast = 256;  // tile non-zeros appended in one go when they fit
+
+template <int R>
+__device__ __forceinline__ void flush_full(uint32_t* qi, float* qv, int& qn, int lane, float* __restrict__ table,
+                                           const HashParams& hp, uint32_t& bad) {
+  __syncwarp();
+  while (qn >= 32) {
+    qn -= 32;
+    const float v = qv[qn + lane];
+    bad |= nonfinite(v);
+    insert_one<R>(qi[qn + lane], v, table, hp);
+  }
+  __syncwarp();
+}
+
 template <int R, int MODE>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 4)
 k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __restrict__ bitmap,
            float* __restrict__ table, unsigned long long* __restrict__ counters,
            const __grid_constant__ HashParams hp) {
-  __shared__ uint32_t s_qi[kWarps][kQCap];
-  __shared__ float s_qv[kWarps][kQCap];
+  constexpr int kCap = 32 + kQFast;
+  __shared__ uint32_t s_qi[kWarps][kCap];
+  __shared__ float s_qv[kWarps][kCap];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   uint32_t* qi = s_qi[wib];
@@ -86,13 +111,15 @@ k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __res
   const int64_t ntiles = (dim + kTile - 1) / kTile;
   const int64_t nelem_words = (dim + 31) / 32;
   const int64_t nw = (int64_t)gridDim.x * kWarps;
-  const uint32_t lt = lanemask_lt();
   const float4* g4 = reinterpret_cast<const float4*>(g);
+  const int src_grp = 8 * (lane & 3);  // transpose: word L gathers lanes 8(L&3)..+7
+  const int src_sh = 4 * (lane >> 2);  //            at nibble k = L>>2
 
-  int qn = 0;                    // warp-uniform queue depth
-  unsigned long long nnz = 0;    // warp-uniform
-  unsigned long long sel = 0;    // per-lane selected coordinates (MODE 2)
+  int qn = 0;                  // warp-uniform queue depth
+  unsigned long long nnz = 0;  // warp-uniform
+  unsigned long long sel = 0;  // per-lane selected coordinates (MODE 2)
   uint32_t bad = 0;
+  float fin = 0.f;  // MODE 2: sum of 0*x, NaN iff a non-finite element was seen
 
   for (int64_t t = (int64_t)blockIdx.x * kWarps + wib; t < ntiles; t += nw) {
     const int64_t base = t * kTile;
@@ -110,68 +137,99 @@ k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __res
         v[k].w = e + 3 < dim ? g[e + 3] : 0.f;
       }
     }
-    uint32_t mword = 0xFFFFFFFFu;  // element-level selection word of elements base+32*lane..
+    // non-zero flags (-0.0 == 0 is not a non-zero, sparse.py:167)
+    uint32_t m = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      m |= ((uint32_t)(v[k].x != 0.f) << (4 * k)) | ((uint32_t)(v[k].y != 0.f) << (4 * k + 1)) |
+           ((uint32_t)(v[k].z != 0.f) << (4 * k + 2)) | ((uint32_t)(v[k].w != 0.f) << (4 * k + 3));
+    }
     if (MODE == 2) {
-      mword = bs == 1 ? ((t * 32 + lane) < nelem_words ? __ldg(bitmap + t * 32 + lane) : 0u)
-                      : expand_blocks(bitmap, base + 32 * lane, dim, bs);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        fin += 0.f * v[k].x + 0.f * v[k].y + 0.f * v[k].z + 0.f * v[k].w;
+      // selection word of elements base+32L..+31, then the inverse transpose into m's layout
+      uint32_t mword = bs == 1 ? ((t * 32 + lane) < nelem_words ? __ldg(bitmap + t * 32 + lane) : 0u)
+                               : expand_blocks(bitmap, base + 32 * lane, dim, bs);
       const int64_t e0 = base + 32 * lane;
       if (e0 + 32 > dim) mword &= e0 >= dim ? 0u : range_mask(0, (int)(dim - e0));
       sel += __popc(mword);
-    }
-    uint32_t myword = 0;  // non-zero word for elements base+32*lane..+31
+      uint32_t msel = 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const float4 x = v[k];
-      bad |= nonfinite(x.x) | nonfinite(x.y) | nonfinite(x.z) | nonfinite(x.w);
-      // -0.0 compares equal to 0 and is not a non-zero (sparse.py:167)
-      uint32_t nib = (uint32_t)(x.x != 0.f) | ((uint32_t)(x.y != 0.f) << 1) |
-                     ((uint32_t)(x.z != 0.f) << 2) | ((uint32_t)(x.w != 0.f) << 3);
-      if (MODE == 2) {
+      for (int k = 0; k < 8; ++k) {
         const uint32_t mk = __shfl_sync(kFull, mword, 4 * k + (lane >> 3));
-        nib &= (mk >> ((lane & 7) * 4)) & 0xFu;
+        msel |= ((mk >> ((lane & 7) * 4)) & 0xFu) << (4 * k);
       }
-      if (__any_sync(kFull, nib)) {
-        // bitmap word 4k + (lane>>3): OR the 8 nibbles of each 8-lane group
-        uint32_t tw = nib << ((lane & 7) * 4);
-        tw |= __shfl_xor_sync(kFull, tw, 1);
-        tw |= __shfl_xor_sync(kFull, tw, 2);
-        tw |= __shfl_xor_sync(kFull, tw, 4);
-        const uint32_t wv = __shfl_sync(kFull, tw, (lane & 3) << 3);
-        if ((lane >> 2) == k) myword = wv;
-        // warp compaction of the non-zeros into the queue
-        const uint32_t b0 = __ballot_sync(kFull, nib & 1u);
-        const uint32_t b1 = __ballot_sync(kFull, nib & 2u);
-        const uint32_t b2 = __ballot_sync(kFull, nib & 4u);
-        const uint32_t b3 = __ballot_sync(kFull, nib & 8u);
-        int pos = qn + __popc(b0 & lt) + __popc(b1 & lt) + __popc(b2 & lt) + __popc(b3 & lt);
-        const int tot = __popc(b0) + __popc(b1) + __popc(b2) + __popc(b3);
-        const uint32_t e0 = (uint32_t)(base + k * 128 + lane * 4);
-        if (nib & 1u) { qi[pos] = e0 + 0; qv[pos] = x.x; ++pos; }
-        if (nib & 2u) { qi[pos] = e0 + 1; qv[pos] = x.y; ++pos; }
-        if (nib & 4u) { qi[pos] = e0 + 2; qv[pos] = x.z; ++pos; }
-        if (nib & 8u) { qi[pos] = e0 + 3; qv[pos] = x.w; ++pos; }
-        qn += tot;
-        nnz += (unsigned)tot;
-        __syncwarp();
-        while (qn >= 32) {
-          qn -= 32;
-          insert_one<R>(qi[qn + lane], qv[qn + lane], table, hp);
+      m &= msel;
+    }
+    const int cnt = __popc(m);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += n;
+    }
+    const int total = __shfl_sync(kFull, incl, 31);
+    uint32_t word = 0;  // MODE 0/1: non-zero word of elements base+32*lane..+31
+    if (total) {
+      if (MODE != 2) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const uint32_t mq = __shfl_sync(kFull, m, src_grp + q);
+          word |= ((mq >> src_sh) & 0xFu) << (4 * q);
         }
-        __syncwarp();
+      }
+      nnz += (unsigned)total;
+      if (qn + total <= kCap) {
+        int pos = qn + incl - cnt;
+        const uint32_t e0 = (uint32_t)(base + lane * 4);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t nib = (m >> (4 * k)) & 0xFu;
+          if (nib) {
+            const uint32_t e = e0 + 128u * k;
+            if (nib & 1u) { qi[pos] = e + 0; qv[pos] = v[k].x; ++pos; }
+            if (nib & 2u) { qi[pos] = e + 1; qv[pos] = v[k].y; ++pos; }
+            if (nib & 4u) { qi[pos] = e + 2; qv[pos] = v[k].z; ++pos; }
+            if (nib & 8u) { qi[pos] = e + 3; qv[pos] = v[k].w; ++pos; }
+          }
+        }
+        qn += total;
+        flush_full<R>(qi, qv, qn, lane, table, hp, bad);
+      } else {
+        // dense tile: append chunk by chunk (<= 128 per chunk), flushing in between
+        const uint32_t lt = lanemask_lt();
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t nib = (m >> (4 * k)) & 0xFu;
+          const uint32_t b0 = __ballot_sync(kFull, nib & 1u);
+          const uint32_t b1 = __ballot_sync(kFull, nib & 2u);
+          const uint32_t b2 = __ballot_sync(kFull, nib & 4u);
+          const uint32_t b3 = __ballot_sync(kFull, nib & 8u);
+          int pos = qn + __popc(b0 & lt) + __popc(b1 & lt) + __popc(b2 & lt) + __popc(b3 & lt);
+          const int tot = __popc(b0) + __popc(b1) + __popc(b2) + __popc(b3);
+          const uint32_t e = (uint32_t)(base + k * 128 + lane * 4);
+          if (nib & 1u) { qi[pos] = e + 0; qv[pos] = v[k].x; ++pos; }
+          if (nib & 2u) { qi[pos] = e + 1; qv[pos] = v[k].y; ++pos; }
+          if (nib & 4u) { qi[pos] = e + 2; qv[pos] = v[k].z; ++pos; }
+          if (nib & 8u) { qi[pos] = e + 3; qv[pos] = v[k].w; ++pos; }
+          qn += tot;
+          flush_full<R>(qi, qv, qn, lane, table, hp, bad);
+        }
       }
     }
     if (MODE == 0) {
       const int64_t wi = t * 32 + lane;
-      if (wi < nelem_words) bitmap[wi] = myword;
+      if (wi < nelem_words) bitmap[wi] = word;
     } else if (MODE == 1) {
-      if (myword) {  // OR the flags of every block this 32-element span touches
+      if (word) {  // OR the flags of every block this 32-element span touches
         const int64_t e0 = base + 32 * lane;
         const int64_t e_end = e0 + 32 < dim ? e0 + 32 : dim;
         int64_t b = e0 / bs, s = e0;
         while (s < e_end) {
           int64_t be = (b + 1) * bs;
           if (be > e_end) be = e_end;
-          if (myword & range_mask((int)(s - e0), (int)(be - e0)))
+          if (word & range_mask((int)(s - e0), (int)(be - e0)))
             atomicOr(bitmap + (b >> 5), 1u << (b & 31));
           s = be;
           ++b;
@@ -180,7 +238,12 @@ k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __res
     }
   }
   __syncwarp();
-  if (lane < qn) insert_one<R>(qi[lane], qv[lane], table, hp);
+  if (lane < qn) {
+    const float v = qv[lane];
+    bad |= nonfinite(v);
+    insert_one<R>(qi[lane], v, table, hp);
+  }
+  if (MODE == 2) bad |= (fin != 0.f);  // NaN != 0
   bad = __any_sync(kFull, bad);
   if (MODE == 2) {
 #pragma unroll
@@ -241,11 +304,34 @@ __device__ __forceinline__ float query_one(uint64_t i, const float* __restrict__
   return lower_median<R>(e);
 }
 
+template <bool BLOCKS>
+__device__ __forceinline__ uint32_t decode_word(const uint32_t* __restrict__ bitmap, int64_t t, int lane,
+                                               int64_t dim, int64_t bs, int64_t nelem_words) {
+  const int64_t e0 = t * kTile + 32 * lane;
+  uint32_t word;
+  if (!BLOCKS) {
+    word = (t * 32 + lane) < nelem_words ? __ldg(bitmap + t * 32 + lane) : 0u;
+  } else {
+    word = expand_blocks(bitmap, e0, dim, bs);
+  }
+  if (e0 + 32 > dim) word &= e0 >= dim ? 0u : range_mask(0, (int)(dim - e0));
+  return word;
+}
+
+// zt/zc: the NEXT reduce's sketch table and counters, zeroed here so that the next
+// compress needs no memset (plan ping-pong, s2_reduce); may be null.
 template <int R, bool BLOCKS>
 __global__ void __launch_bounds__(kThreads)
 k_decode(const uint32_t* __restrict__ bitmap, int64_t dim, int64_t bs,
-         const float* __restrict__ table, float workers, float* __restrict__ out,
-         const __grid_constant__ HashParams hp) {
+         const float* __restrict__ table, float workers, float inv_workers, int workers_pow2,
+         float* __restrict__ out, float4* __restrict__ zt, int64_t zt_n4,
+         unsigned long long* __restrict__ zc, const __grid_constant__ HashParams hp) {
+  if (zt != nullptr) {
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < zt_n4; i += (int64_t)gridDim.x * kThreads)
+      zt[i] = z;
+  }
+  if (zc != nullptr && blockIdx.x == 0 && threadIdx.x < S2_NUM_COUNTERS) zc[threadIdx.x] = 0ull;
   __shared__ uint16_t s_q[kWarps][kTile];
   __shared__ __align__(16) float s_v[kWarps][kTile];
   const int lane = threadIdx.x & 31;
@@ -256,16 +342,12 @@ k_decode(const uint32_t* __restrict__ bitmap, int64_t dim, int64_t bs,
   const int64_t nelem_words = (dim + 31) / 32;
   const int64_t nw = (int64_t)gridDim.x * kWarps;
 
-  for (int64_t t = (int64_t)blockIdx.x * kWarps + wib; t < ntiles; t += nw) {
+  int64_t t = (int64_t)blockIdx.x * kWarps + wib;
+  uint32_t wnext = t < ntiles ? decode_word<BLOCKS>(bitmap, t, lane, dim, bs, nelem_words) : 0u;
+  for (; t < ntiles; t += nw) {
     const int64_t base = t * kTile;
-    const int64_t e0 = base + 32 * lane;
-    uint32_t word;
-    if (!BLOCKS) {
-      word = (t * 32 + lane) < nelem_words ? __ldg(bitmap + t * 32 + lane) : 0u;
-    } else {
-      word = expand_blocks(bitmap, e0, dim, bs);
-    }
-    if (e0 + 32 > dim) word &= e0 >= dim ? 0u : range_mask(0, (int)(dim - e0));
+    const uint32_t word = wnext;  // prefetched one tile ahead
+    if (t + nw < ntiles) wnext = decode_word<BLOCKS>(bitmap, t + nw, lane, dim, bs, nelem_words);
     // warp exclusive scan of the per-lane set counts -> queue of set positions
     const int cnt = __popc(word);
     int pre = cnt;
@@ -281,7 +363,8 @@ k_decode(const uint32_t* __restrict__ bitmap, int64_t dim, int64_t bs,
     for (int s = lane; s < total; s += 32) {
       const int pos = q[s];
       // IEEE division: sparse.py:213 divides the float64 query by workers
-      vals[pos] = __fdiv_rn(query_one<R>((uint64_t)(base + pos), table, hp), workers);
+      const float qv = query_one<R>((uint64_t)(base + pos), table, hp);
+      vals[pos] = workers_pow2 ? qv * inv_workers : __fdiv_rn(qv, workers);  // x*2^-k is exact
     }
     __syncwarp();
     const bool full = base + kTile <= dim;
@@ -545,11 +628,14 @@ static void launch_compress_r(const Plan& p, const float* g, uint32_t* bitmap, f
 }
 
 cudaError_t launch_compress(const Plan& p, const float* g, uint32_t* bitmap, float* table,
-                            unsigned long long* counters, int mode, cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(table, 0, sizeof(float) * (size_t)p.hp.rows * p.hp.cols, st);
-  if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(counters, 0, sizeof(unsigned long long) * S2_NUM_COUNTERS, st);
-  if (e != cudaSuccess) return e;
+                            unsigned long long* counters, int mode, cudaStream_t st, bool prezeroed) {
+  cudaError_t e = cudaSuccess;
+  if (!prezeroed) {
+    e = cudaMemsetAsync(table, 0, sizeof(float) * (size_t)p.hp.rows * p.hp.cols, st);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(counters, 0, sizeof(unsigned long long) * S2_NUM_COUNTERS, st);
+    if (e != cudaSuccess) return e;
+  }
   if (mode == S2_MASK_NONZERO && p.block_size > 1) {
     e = cudaMemsetAsync(bitmap, 0, sizeof(uint32_t) * (size_t)p.words, st);
     if (e != cudaSuccess) return e;
@@ -570,34 +656,29 @@ cudaError_t launch_compress(const Plan& p, const float* g, uint32_t* bitmap, flo
 
 template <int R>
 static void launch_decode_r(const Plan& p, const uint32_t* bitmap, const float* table, int workers,
-                            float* out, cudaStream_t st) {
+                            float* out, float* zt, unsigned long long* zc, cudaStream_t st) {
   const int64_t ntiles = (p.dim + kTile - 1) / kTile;
   const int grid = grid_for(ntiles, 4);
+  const int pow2 = (workers & (workers - 1)) == 0;
+  const float inv = 1.0f / (float)workers;
+  const int64_t zn4 = zt ? ((int64_t)p.hp.rows * p.hp.cols + 3) / 4 : 0;
+  float4* z4 = reinterpret_cast<float4*>(zt);
   if (p.block_size == 1)
-    k_decode<R, false><<<grid, kThreads, 0, st>>>(bitmap, p.dim, 1, table, (float)workers, out, p.hp);
+    k_decode<R, false><<<grid, kThreads, 0, st>>>(bitmap, p.dim, 1, table, (float)workers, inv, pow2, out, z4,
+                                                  zn4, zc, p.hp);
   else
-    k_decode<R, true><<<grid, kThreads, 0, st>>>(bitmap, p.dim, p.block_size, table, (float)workers, out, p.hp);
+    k_decode<R, true><<<grid, kThreads, 0, st>>>(bitmap, p.dim, p.block_size, table, (float)workers, inv, pow2,
+                                                 out, z4, zn4, zc, p.hp);
 }
 
 cudaError_t launch_decode(const Plan& p, const uint32_t* bitmap, const float* table, int workers,
-                          float* out, cudaStream_t st) {
+                          float* out, cudaStream_t st, float* zero_table, unsigned long long* zero_counters) {
   switch (p.hp.rows) {
-    case 1: launch_decode_r<1>(p, bitmap, table, workers, out, st); break;
-    case 2: launch_decode_r<2>(p, bitmap, table, workers, out, st); break;
-    case 3: launch_decode_r<3>(p, bitmap, table, workers, out, st); break;
-    case 4: launch_decode_r<4>(p, bitmap, table, workers, out, st); break;
-    case 5: launch_decode_r<5>(p, bitmap, table, workers, out, st); break;
-    case 6: launch_decode_r<6>(p, bitmap, table, workers, out, st); break;
-    case 7: launch_decode_r<7>(p, bitmap, table, workers, out, st); break;
-    case 8: launch_decode_r<8>(p, bitmap, table, workers, out, st); break;
-    case 9: launch_decode_r<9>(p, bitmap, table, workers, out, st); break;
-    case 10: launch_decode_r<10>(p, bitmap, table, workers, out, st); break;
-    case 11: launch_decode_r<11>(p, bitmap, table, workers, out, st); break;
-    case 12: launch_decode_r<12>(p, bitmap, table, workers, out, st); break;
-    case 13: launch_decode_r<13>(p, bitmap, table, workers, out, st); break;
-    case 14: launch_decode_r<14>(p, bitmap, table, workers, out, st); break;
-    case 15: launch_decode_r<15>(p, bitmap, table, workers, out, st); break;
-    case 16: launch_decode_r<16>(p, bitmap, table, workers, out, st); break;
+#define S2_CASE(r) \
+  case r: launch_decode_r<r>(p, bitmap, table, workers, out, zero_table, zero_counters, st); break;
+    S2_CASE(1) S2_CASE(2) S2_CASE(3) S2_CASE(4) S2_CASE(5) S2_CASE(6) S2_CASE(7) S2_CASE(8)
+    S2_CASE(9) S2_CASE(10) S2_CASE(11) S2_CASE(12) S2_CASE(13) S2_CASE(14) S2_CASE(15) S2_CASE(16)
+#undef S2_CASE
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

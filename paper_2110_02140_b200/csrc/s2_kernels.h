@@ -20,9 +20,10 @@ struct Plan {
 };
 
 cudaError_t launch_compress(const Plan& p, const float* g, uint32_t* bitmap, float* table,
-                            unsigned long long* counters, int mode, cudaStream_t st);
+                            unsigned long long* counters, int mode, cudaStream_t st, bool prezeroed = false);
 cudaError_t launch_decode(const Plan& p, const uint32_t* bitmap, const float* table, int workers,
-                          float* out, cudaStream_t st);
+                          float* out, cudaStream_t st, float* zero_table = nullptr,
+                          unsigned long long* zero_counters = nullptr);
 cudaError_t launch_bitmap_or(int64_t words, const uint32_t* stacked, int nmasks, uint32_t* out,
                              cudaStream_t st);
 cudaError_t launch_table_sum(int64_t cells, const float* stacked, int ntables, float* out,

@@ -60,7 +60,6 @@ class S2Reducer:
             ctypes.memmove(uid, box[0], 128)
         check(lib.s2_comm_init(self.plan.handle, self.world, self.rank, uid), "comm init")
         check(lib.s2_comm_check(self.plan.handle, stream_ptr()), "comm check")
-        self.counters = torch.zeros(S2_NUM_COUNTERS, dtype=torch.int64, device=self.device)
 
     def reduce(self, g: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         """Averaged gradient estimate: median-of-rows sketch query ÷ world at every union-bitmap
@@ -71,13 +70,19 @@ class S2Reducer:
             g = as_gradient(g, self.device)
         if out is None:
             out = torch.empty(self.dim, dtype=torch.float32, device=self.device)
-        check(lib.s2_reduce(self.plan.handle, ptr(g), ptr(out), ptr(self.counters), stream_ptr(stream)), "reduce")
+        check(lib.s2_reduce(self.plan.handle, ptr(g), ptr(out), None, stream_ptr(stream)), "reduce")
         return out
+
+    def counters(self) -> list[int]:
+        """Counters of the last reduce (synchronises the current stream): [nnz, nonfinite, selected, 0]."""
+        host = (ctypes.c_uint64 * S2_NUM_COUNTERS)()
+        check(lib.s2_read_counters(self.plan.handle, host, stream_ptr()), "counters")
+        return [int(v) for v in host]
 
     def check_finite(self) -> None:
         """Raise the reference's ValueError if the last reduced gradient held NaN/Inf (syncs)."""
-        if int(self.counters[S2_CNT_NONFINITE]):
+        if self.counters()[S2_CNT_NONFINITE]:
             raise ValueError("gradient vector contains NaN or Inf")
 
     def last_nnz(self) -> int:
-        return int(self.counters[S2_CNT_NNZ])
+        return self.counters()[S2_CNT_NNZ]

@@ -172,12 +172,14 @@ def test_reducer_single_gpu_equals_compress_decode(s2):
     import torch
 
     d = 1_000_000
-    g = o.synthetic_gradient(d, 0.01, 0, kind="int")
     red = s2.S2Reducer(d, rows=3, cols=16384, seed=0)
-    out = host(red.reduce(cuda(g)))
-    ref = o.decompress(o.compress(g, g != 0, 3, 16384, 0))
-    assert np.array_equal(out, ref.astype(np.float32))
-    assert red.last_nnz() == int((g != 0).sum())
+    # consecutive reduces alternate the plan's ping-pong tables (decode i zeroes table i+1)
+    for k, alpha in enumerate((0.01, 0.05, 0.001, 0.02, 0.0)):
+        g = o.synthetic_gradient(d, alpha, k, kind="int")
+        out = host(red.reduce(cuda(g)))
+        ref = o.decompress(o.compress(g, g != 0, 3, 16384, 0))
+        assert np.array_equal(out, ref.astype(np.float32)), k
+        assert red.last_nnz() == int((g != 0).sum())
     red.check_finite()
     bad = g.copy()
     bad[17] = np.inf
