@@ -20,6 +20,7 @@
 // table float32[rows][cols] row-major.  A warp tile is 1024 elements = 32
 // bitmap words = 8 float4 per lane.
 #include <cstdio>
+#include <cstdlib>
 
 #include "s2_common.cuh"
 #include "s2_kernels.h"
@@ -96,8 +97,29 @@ __device__ __forceinline__ void flush_full(uint32_t* qi, float* qv, int& qn, int
   __syncwarp();
 }
 
-template <int R, int MODE>
-__global__ void __launch_bounds__(kThreads, 4)
+__device__ __forceinline__ void load_tile(float4 (&v)[8], const float* __restrict__ g, int64_t t, int64_t dim,
+                                          int lane) {
+  const int64_t base = t * kTile;
+  if (base + kTile <= dim) {
+    const float4* g4 = reinterpret_cast<const float4*>(g) + (base >> 2) + lane;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __ldcs(g4 + k * 32);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int64_t e = base + k * 128 + lane * 4;
+      v[k].x = e + 0 < dim ? g[e + 0] : 0.f;
+      v[k].y = e + 1 < dim ? g[e + 1] : 0.f;
+      v[k].z = e + 2 < dim ? g[e + 2] : 0.f;
+      v[k].w = e + 3 < dim ? g[e + 3] : 0.f;
+    }
+  }
+}
+
+// MINB: min CTAs per SM (register budget).  The next tile's 8 loads are issued before
+// the current tile is processed, so a warp always has 4 KB of loads in flight.
+template <int R, int MODE, int MINB = 2>
+__global__ void __launch_bounds__(kThreads, MINB)
 k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __restrict__ bitmap,
            float* __restrict__ table, unsigned long long* __restrict__ counters,
            const __grid_constant__ HashParams hp) {
@@ -111,7 +133,6 @@ k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __res
   const int64_t ntiles = (dim + kTile - 1) / kTile;
   const int64_t nelem_words = (dim + 31) / 32;
   const int64_t nw = (int64_t)gridDim.x * kWarps;
-  const float4* g4 = reinterpret_cast<const float4*>(g);
   const int src_grp = 8 * (lane & 3);  // transpose: word L gathers lanes 8(L&3)..+7
   const int src_sh = 4 * (lane >> 2);  //            at nibble k = L>>2
 
@@ -121,22 +142,16 @@ k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __res
   uint32_t bad = 0;
   float fin = 0.f;  // MODE 2: sum of 0*x, NaN iff a non-finite element was seen
 
-  for (int64_t t = (int64_t)blockIdx.x * kWarps + wib; t < ntiles; t += nw) {
+  int64_t t = (int64_t)blockIdx.x * kWarps + wib;
+  float4 vn[8];
+  if (t < ntiles) load_tile(vn, g, t, dim, lane);
+#pragma unroll 2
+  for (; t < ntiles; t += nw) {
     const int64_t base = t * kTile;
     float4 v[8];
-    if (base + kTile <= dim) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] = __ldcs(g4 + (base >> 2) + k * 32 + lane);
-    } else {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int64_t e = base + k * 128 + lane * 4;
-        v[k].x = e + 0 < dim ? g[e + 0] : 0.f;
-        v[k].y = e + 1 < dim ? g[e + 1] : 0.f;
-        v[k].z = e + 2 < dim ? g[e + 2] : 0.f;
-        v[k].w = e + 3 < dim ? g[e + 3] : 0.f;
-      }
-    }
+    for (int k = 0; k < 8; ++k) v[k] = vn[k];
+    if (t + nw < ntiles) load_tile(vn, g, t + nw, dim, lane);
     // non-zero flags (-0.0 == 0 is not a non-zero, sparse.py:167)
     uint32_t m = 0;
 #pragma unroll
@@ -613,17 +628,37 @@ static int grid_for(int64_t ntiles, int ctas_per_sm) {
   return gr < 1 ? 1 : (int)gr;
 }
 
+static int compress_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("S2_COMPRESS_MINB");
+    v = e ? atoi(e) : 2;
+    if (v != 2 && v != 3 && v != 4) v = 2;
+  }
+  return v;
+}
+
+template <int R, int MINB>
+static void launch_compress_rm(const Plan& p, const float* g, uint32_t* bitmap, float* table,
+                               unsigned long long* counters, int mode, cudaStream_t st) {
+  const int64_t ntiles = (p.dim + kTile - 1) / kTile;
+  const int grid = grid_for(ntiles, MINB);
+  if (mode == S2_MASK_GIVEN) {
+    k_compress<R, 2, MINB><<<grid, kThreads, 0, st>>>(g, p.dim, p.block_size, bitmap, table, counters, p.hp);
+  } else if (p.block_size == 1) {
+    k_compress<R, 0, MINB><<<grid, kThreads, 0, st>>>(g, p.dim, p.block_size, bitmap, table, counters, p.hp);
+  } else {
+    k_compress<R, 1, MINB><<<grid, kThreads, 0, st>>>(g, p.dim, p.block_size, bitmap, table, counters, p.hp);
+  }
+}
+
 template <int R>
 static void launch_compress_r(const Plan& p, const float* g, uint32_t* bitmap, float* table,
                               unsigned long long* counters, int mode, cudaStream_t st) {
-  const int64_t ntiles = (p.dim + kTile - 1) / kTile;
-  const int grid = grid_for(ntiles, 4);
-  if (mode == S2_MASK_GIVEN) {
-    k_compress<R, 2><<<grid, kThreads, 0, st>>>(g, p.dim, p.block_size, bitmap, table, counters, p.hp);
-  } else if (p.block_size == 1) {
-    k_compress<R, 0><<<grid, kThreads, 0, st>>>(g, p.dim, p.block_size, bitmap, table, counters, p.hp);
-  } else {
-    k_compress<R, 1><<<grid, kThreads, 0, st>>>(g, p.dim, p.block_size, bitmap, table, counters, p.hp);
+  switch (compress_variant()) {
+    case 3: launch_compress_rm<R, 3>(p, g, bitmap, table, counters, mode, st); break;
+    case 4: launch_compress_rm<R, 4>(p, g, bitmap, table, counters, mode, st); break;
+    default: launch_compress_rm<R, 2>(p, g, bitmap, table, counters, mode, st); break;
   }
 }
 
