@@ -30,7 +30,6 @@ namespace s2 {
 constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
 constexpr int kTile = 1024;
-constexpr int kQCap = 32 + 128;
 
 static int g_num_sms = 0;
 static int num_sms() {
@@ -82,7 +81,7 @@ __device__ __forceinline__ void insert_one(uint64_t i, float v, float* __restric
 // from one warp scan of popc(m); every full batch of 32 is hashed and inserted by
 // the 32 lanes together.  NaN/Inf are non-zeros, so finiteness is tested on the
 // queue only (MODE 2 tests every element: unselected non-zeros never reach the queue).
-constexpr int kQFast = 256;  // tile non-zeros appended in one go when they fit
+constexpr int kQFast = 128;  // tile non-zeros appended in one go when they fit
 
 template <int R>
 __device__ __forceinline__ void flush_full(uint32_t* qi, float* qv, int& qn, int lane, float* __restrict__ table,
@@ -116,21 +115,69 @@ __device__ __forceinline__ void load_tile(float4 (&v)[8], const float* __restric
   }
 }
 
-// MINB: min CTAs per SM (register budget).  The next tile's 8 loads are issued before
-// the current tile is processed, so a warp always has 4 KB of loads in flight.
-template <int R, int MODE, int MINB = 2>
-__global__ void __launch_bounds__(kThreads, MINB)
+// ---- TMA (cp.async.bulk) + mbarrier helpers -------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// order this thread's prior generic-proxy shared accesses before later async-proxy (TMA) ones
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+// one elected lane: arm the barrier with the byte count and start a 1D bulk copy global -> smem
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                            uint64_t pol) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+          "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "S2_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra S2_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// LOAD 0: the next tile's 8 float4 per lane are loaded into registers before the current
+//         tile is processed (needs ~127 registers -> 2 CTAs/SM).
+// LOAD 1: the next tile (4 KB) is prefetched into a per-warp shared buffer by one TMA bulk
+//         copy (cp.async.bulk + mbarrier) right after the current tile has been moved to
+//         registers, so prefetch costs no registers and 4 CTAs (32 warps) fit per SM.
+template <int R, int MODE, int LOAD>
+__global__ void __launch_bounds__(kThreads, LOAD == 0 ? 2 : 4)
 k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __restrict__ bitmap,
            float* __restrict__ table, unsigned long long* __restrict__ counters,
            const __grid_constant__ HashParams hp) {
   constexpr int kCap = 32 + kQFast;
   __shared__ uint32_t s_qi[kWarps][kCap];
   __shared__ float s_qv[kWarps][kCap];
+  __shared__ __align__(128) float4 s_tile[LOAD == 1 ? kWarps : 1][kTile / 4];
+  __shared__ __align__(8) uint64_t s_bar[kWarps];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   uint32_t* qi = s_qi[wib];
   float* qv = s_qv[wib];
   const int64_t ntiles = (dim + kTile - 1) / kTile;
+  const int64_t nfull = dim / kTile;  // tiles that TMA can move whole
   const int64_t nelem_words = (dim + 31) / 32;
   const int64_t nw = (int64_t)gridDim.x * kWarps;
   const int src_grp = 8 * (lane & 3);  // transpose: word L gathers lanes 8(L&3)..+7
@@ -143,21 +190,51 @@ k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __res
   float fin = 0.f;  // MODE 2: sum of 0*x, NaN iff a non-finite element was seen
 
   int64_t t = (int64_t)blockIdx.x * kWarps + wib;
-  float4 vn[8];
-  if (t < ntiles) load_tile(vn, g, t, dim, lane);
-#pragma unroll 2
+  float4 vn[LOAD == 0 ? 8 : 1];
+  uint32_t parity = 0;
+  uint64_t pol = 0;
+  if (LOAD == 0) {
+    if (t < ntiles) load_tile(*reinterpret_cast<float4(*)[8]>(vn), g, t, dim, lane);
+  } else {
+    if (lane == 0) {
+      mbar_init(&s_bar[wib], 1);
+      fence_barrier_init();
+    }
+    __syncwarp();
+    pol = policy_evict_first();
+    if (lane == 0 && t < nfull) tma_load_1d(s_tile[wib], g + t * kTile, kTile * 4, &s_bar[wib], pol);
+  }
+#pragma unroll 1
   for (; t < ntiles; t += nw) {
     const int64_t base = t * kTile;
     float4 v[8];
+    if (LOAD == 0) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = vn[k];
-    if (t + nw < ntiles) load_tile(vn, g, t + nw, dim, lane);
+      for (int k = 0; k < 8; ++k) v[k] = vn[k < (LOAD == 0 ? 8 : 1) ? k : 0];
+      if (t + nw < ntiles) load_tile(*reinterpret_cast<float4(*)[8]>(vn), g, t + nw, dim, lane);
+    } else {
+      if (t < nfull) {
+        mbar_wait(&s_bar[wib], parity);
+        parity ^= 1u;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = s_tile[wib][k * 32 + lane];
+      } else {
+        load_tile(v, g, t, dim, lane);  // ragged last tile
+      }
+    }
     // non-zero flags (-0.0 == 0 is not a non-zero, sparse.py:167)
     uint32_t m = 0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       m |= ((uint32_t)(v[k].x != 0.f) << (4 * k)) | ((uint32_t)(v[k].y != 0.f) << (4 * k + 1)) |
            ((uint32_t)(v[k].z != 0.f) << (4 * k + 2)) | ((uint32_t)(v[k].w != 0.f) << (4 * k + 3));
+    }
+    if (LOAD == 1) {
+      // every lane has consumed its shared-tile reads (m depends on all of v): release the
+      // buffer to the async proxy and prefetch the next tile while this one is processed
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0 && t + nw < nfull) tma_load_1d(s_tile[wib], g + (t + nw) * kTile, kTile * 4, &s_bar[wib], pol);
     }
     if (MODE == 2) {
 #pragma unroll
@@ -628,38 +705,35 @@ static int grid_for(int64_t ntiles, int ctas_per_sm) {
   return gr < 1 ? 1 : (int)gr;
 }
 
-static int compress_variant() {
+static int compress_variant() {  // S2_COMPRESS_LOAD=0 (register prefetch) | 1 (TMA prefetch, default)
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("S2_COMPRESS_MINB");
-    v = e ? atoi(e) : 2;
-    if (v != 2 && v != 3 && v != 4) v = 2;
+    const char* e = getenv("S2_COMPRESS_LOAD");
+    v = e ? atoi(e) : 1;
+    if (v != 0 && v != 1) v = 1;
   }
   return v;
 }
 
-template <int R, int MINB>
+template <int R, int LOAD>
 static void launch_compress_rm(const Plan& p, const float* g, uint32_t* bitmap, float* table,
                                unsigned long long* counters, int mode, cudaStream_t st) {
   const int64_t ntiles = (p.dim + kTile - 1) / kTile;
-  const int grid = grid_for(ntiles, MINB);
+  const int grid = grid_for(ntiles, LOAD == 0 ? 2 : 4);
   if (mode == S2_MASK_GIVEN) {
-    k_compress<R, 2, MINB><<<grid, kThreads, 0, st>>>(g, p.dim, p.block_size, bitmap, table, counters, p.hp);
+    k_compress<R, 2, LOAD><<<grid, kThreads, 0, st>>>(g, p.dim, p.block_size, bitmap, table, counters, p.hp);
   } else if (p.block_size == 1) {
-    k_compress<R, 0, MINB><<<grid, kThreads, 0, st>>>(g, p.dim, p.block_size, bitmap, table, counters, p.hp);
+    k_compress<R, 0, LOAD><<<grid, kThreads, 0, st>>>(g, p.dim, p.block_size, bitmap, table, counters, p.hp);
   } else {
-    k_compress<R, 1, MINB><<<grid, kThreads, 0, st>>>(g, p.dim, p.block_size, bitmap, table, counters, p.hp);
+    k_compress<R, 1, LOAD><<<grid, kThreads, 0, st>>>(g, p.dim, p.block_size, bitmap, table, counters, p.hp);
   }
 }
 
 template <int R>
 static void launch_compress_r(const Plan& p, const float* g, uint32_t* bitmap, float* table,
                               unsigned long long* counters, int mode, cudaStream_t st) {
-  switch (compress_variant()) {
-    case 3: launch_compress_rm<R, 3>(p, g, bitmap, table, counters, mode, st); break;
-    case 4: launch_compress_rm<R, 4>(p, g, bitmap, table, counters, mode, st); break;
-    default: launch_compress_rm<R, 2>(p, g, bitmap, table, counters, mode, st); break;
-  }
+  if (compress_variant() == 0) launch_compress_rm<R, 0>(p, g, bitmap, table, counters, mode, st);
+  else launch_compress_rm<R, 1>(p, g, bitmap, table, counters, mode, st);
 }
 
 cudaError_t launch_compress(const Plan& p, const float* g, uint32_t* bitmap, float* table,

@@ -26,7 +26,7 @@ def timeit(fn, nbytes, reps=200):
 
 
 acc = torch.empty((), device="cuda")
-res["read_sum"] = timeit(lambda i: torch.sum(bufs[i % 4], out=acc), 4 * n)
+res["read_sum"] = timeit(lambda i: torch.sum(bufs[i % 4], dim=0, out=acc), 4 * n)
 res["write_fill"] = timeit(lambda i: outs[i % 4].fill_(0.0), 4 * n)
 res["copy"] = timeit(lambda i: outs[i % 4].copy_(bufs[i % 4]), 8 * n)
 res["memset"] = timeit(lambda i: outs[i % 4].zero_(), 4 * n)
