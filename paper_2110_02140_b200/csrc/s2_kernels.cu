@@ -349,6 +349,182 @@ k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __res
   }
 }
 
+// ------------------------------------------- compress, TMA-staged variant (default)
+//
+// Each warp owns a 2-stage ring of 4 KB shared tiles filled by cp.async.bulk (one
+// elected lane, completion on a per-stage mbarrier), so a warp has up to two tiles
+// (8 KB) in flight with no register cost.  Lane L reads ITS OWN 32 consecutive
+// elements (base+32L..+31) from the staged tile — 8 LDS.128 with an XOR swizzle
+// (chunk (k+L)&7 at step k) so the 8 lanes of each shared-memory phase hit 8
+// different 16-byte bank groups — which makes its non-zero word m exactly bitmap
+// word t*32+L: no transpose.  Non-zeros are appended to the per-warp queue by a
+// loop over the set bits of m, reading values straight from the staged tile
+// (~2 iterations per tile at 1% density instead of 32 per-element predicates).
+constexpr int kTWarps = 4;             // warps per CTA
+constexpr int kTStages = 2;            // tiles in flight per warp
+constexpr int kTCap = 32 + 256;        // queue entries per warp
+constexpr int kTSmemWarp = kTStages * kTile * 4 + kTCap * 8;
+constexpr int kTSmemBytes = kTWarps * kTSmemWarp + kTWarps * kTStages * 8;
+
+template <int R, int MODE>
+__global__ void __launch_bounds__(kTWarps * 32, 5)
+k_compress_tma(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __restrict__ bitmap,
+               float* __restrict__ table, unsigned long long* __restrict__ counters,
+               const __grid_constant__ HashParams hp) {
+  extern __shared__ __align__(128) unsigned char s_raw[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  float* tiles = reinterpret_cast<float*>(s_raw + wib * kTSmemWarp);  // [kTStages][kTile]
+  uint32_t* qi = reinterpret_cast<uint32_t*>(s_raw + wib * kTSmemWarp + kTStages * kTile * 4);
+  float* qv = reinterpret_cast<float*>(qi + kTCap);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_raw + kTWarps * kTSmemWarp) + wib * kTStages;
+
+  const int64_t ntiles = (dim + kTile - 1) / kTile;
+  const int64_t nfull = dim / kTile;
+  const int64_t nelem_words = (dim + 31) / 32;
+  const int64_t nw = (int64_t)gridDim.x * kTWarps;
+  const uint64_t pol = policy_evict_first();
+
+  if (lane == 0) {
+    for (int s = 0; s < kTStages; ++s) mbar_init(&bars[s], 1);
+    fence_barrier_init();
+  }
+  __syncwarp();
+  int64_t t = (int64_t)blockIdx.x * kTWarps + wib;
+  if (lane == 0) {
+    for (int s = 0; s < kTStages; ++s) {
+      const int64_t ts = t + s * nw;
+      if (ts < nfull) tma_load_1d(tiles + s * kTile, g + ts * kTile, kTile * 4, &bars[s], pol);
+    }
+  }
+
+  int qn = 0;
+  unsigned long long nnz = 0;
+  unsigned long long sel = 0;
+  uint32_t bad = 0;
+  float fin = 0.f;
+  uint32_t parity = 0;  // bit s: phase of stage s
+  int stage = 0;
+
+#pragma unroll 1
+  for (; t < ntiles; t += nw) {
+    const int64_t base = t * kTile;
+    float* tile = tiles + stage * kTile;
+    if (t < nfull) {
+      mbar_wait(&bars[stage], (parity >> stage) & 1u);
+      parity ^= 1u << stage;
+    } else {
+      // ragged last tile: zero-filled copy through the generic proxy (no TMA in flight here)
+      for (int e = lane; e < kTile; e += 32) tile[e] = base + e < dim ? g[base + e] : 0.f;
+      __syncwarp();
+    }
+    // lane L: elements 32L..32L+31 of the tile, chunk c = (k + L) & 7 at step k
+    uint32_t m = 0;
+    const float4* row = reinterpret_cast<const float4*>(tile + 32 * lane);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int c = (k + lane) & 7;
+      const float4 x = row[c];
+      const uint32_t nib = (uint32_t)(x.x != 0.f) | ((uint32_t)(x.y != 0.f) << 1) |
+                           ((uint32_t)(x.z != 0.f) << 2) | ((uint32_t)(x.w != 0.f) << 3);
+      m |= nib << (4 * c);
+      if (MODE == 2) fin += 0.f * x.x + 0.f * x.y + 0.f * x.z + 0.f * x.w;
+    }
+    const int64_t e0 = base + 32 * lane;
+    if (MODE == 2) {
+      uint32_t mword = bs == 1 ? ((t * 32 + lane) < nelem_words ? __ldg(bitmap + t * 32 + lane) : 0u)
+                               : expand_blocks(bitmap, e0, dim, bs);
+      if (e0 + 32 > dim) mword &= e0 >= dim ? 0u : range_mask(0, (int)(dim - e0));
+      sel += __popc(mword);
+      m &= mword;
+    }
+    const uint32_t word = m;  // MODE 0/1: the bitmap word of elements e0..e0+31
+    const int cnt = __popc(m);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += n;
+    }
+    const int total = __shfl_sync(kFull, incl, 31);
+    nnz += (unsigned)total;
+    if (qn + total <= kTCap) {
+      int pos = qn + incl - cnt;
+      for (uint32_t mm = m; mm; mm &= mm - 1u) {
+        const int b = __ffs(mm) - 1;
+        qi[pos] = (uint32_t)(e0 + b);
+        qv[pos] = tile[32 * lane + b];
+        ++pos;
+      }
+      qn += total;
+    } else {
+      // very dense tile: drain in rounds of at most kTCap - 32 entries
+      int done = 0;  // entries of this tile already queued (warp-uniform)
+      uint32_t mm = m;
+      int mine = incl - cnt;  // my first rank within the tile
+      while (done < total) {
+        const int room = kTCap - qn;
+        // queue my entries whose tile rank falls in [done, done + room)
+        while (mm && mine < done + room) {
+          const int b = __ffs(mm) - 1;
+          const int pos = qn + (mine - done);
+          qi[pos] = (uint32_t)(e0 + b);
+          qv[pos] = tile[32 * lane + b];
+          mm &= mm - 1u;
+          ++mine;
+        }
+        const int take = total - done < room ? total - done : room;
+        qn += take;
+        done += take;
+        flush_full<R>(qi, qv, qn, lane, table, hp, bad);
+      }
+    }
+    // this tile's shared reads are done: hand the buffer back to the async proxy and
+    // refill it with the tile kTStages rounds ahead
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      const int64_t tn = t + kTStages * nw;
+      if (tn < nfull) tma_load_1d(tile, g + tn * kTile, kTile * 4, &bars[stage], pol);
+    }
+    stage = stage + 1 == kTStages ? 0 : stage + 1;
+    if (MODE == 0) {
+      if (t * 32 + lane < nelem_words) bitmap[t * 32 + lane] = word;
+    } else if (MODE == 1) {
+      if (word) {
+        const int64_t e_end = e0 + 32 < dim ? e0 + 32 : dim;
+        int64_t b = e0 / bs, s = e0;
+        while (s < e_end) {
+          int64_t be = (b + 1) * bs;
+          if (be > e_end) be = e_end;
+          if (word & range_mask((int)(s - e0), (int)(be - e0))) atomicOr(bitmap + (b >> 5), 1u << (b & 31));
+          s = be;
+          ++b;
+        }
+      }
+    }
+    flush_full<R>(qi, qv, qn, lane, table, hp, bad);
+  }
+  __syncwarp();
+  if (lane < qn) {
+    const float v = qv[lane];
+    bad |= nonfinite(v);
+    insert_one<R>(qi[lane], v, table, hp);
+  }
+  if (MODE == 2) bad |= (fin != 0.f);
+  bad = __any_sync(kFull, bad);
+  if (MODE == 2) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sel += __shfl_xor_sync(kFull, sel, o);
+  }
+  if (lane == 0) {
+    if (nnz) atomicAdd(counters + S2_CNT_NNZ, nnz);
+    if (MODE == 0 && nnz) atomicAdd(counters + S2_CNT_SELECTED, nnz);
+    if (MODE == 2 && sel) atomicAdd(counters + S2_CNT_SELECTED, sel);
+    if (bad) atomicOr(counters + S2_CNT_NONFINITE, 1ull);
+  }
+}
+
 // ---------------------------------------------------------------- decode (K4)
 
 // lower median (element (R-1)/2 of the sorted estimates, sketch.py:127-128)
@@ -705,12 +881,13 @@ static int grid_for(int64_t ntiles, int ctas_per_sm) {
   return gr < 1 ? 1 : (int)gr;
 }
 
-static int compress_variant() {  // S2_COMPRESS_LOAD=0 (register prefetch) | 1 (TMA prefetch, default)
+// S2_COMPRESS_LOAD: 0 register prefetch | 1 TMA, coalesced layout | 2 TMA-staged, swizzled (default)
+static int compress_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("S2_COMPRESS_LOAD");
-    v = e ? atoi(e) : 1;
-    if (v != 0 && v != 1) v = 1;
+    v = e ? atoi(e) : 2;
+    if (v < 0 || v > 2) v = 2;
   }
   return v;
 }
@@ -729,11 +906,35 @@ static void launch_compress_rm(const Plan& p, const float* g, uint32_t* bitmap, 
   }
 }
 
+template <int R, int MODE>
+static void launch_compress_tma(const Plan& p, const float* g, uint32_t* bitmap, float* table,
+                                unsigned long long* counters, cudaStream_t st) {
+  static bool attr = false;  // per instantiation
+  if (!attr) {
+    cudaFuncSetAttribute(k_compress_tma<R, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTSmemBytes);
+    attr = true;
+  }
+  const int64_t ntiles = (p.dim + kTile - 1) / kTile;
+  int64_t grid = (ntiles + kTWarps - 1) / kTWarps;
+  const int64_t cap = (int64_t)num_sms() * 5;
+  if (grid > cap) grid = cap;
+  k_compress_tma<R, MODE><<<(int)grid, kTWarps * 32, kTSmemBytes, st>>>(g, p.dim, p.block_size, bitmap, table,
+                                                                        counters, p.hp);
+}
+
 template <int R>
 static void launch_compress_r(const Plan& p, const float* g, uint32_t* bitmap, float* table,
                               unsigned long long* counters, int mode, cudaStream_t st) {
-  if (compress_variant() == 0) launch_compress_rm<R, 0>(p, g, bitmap, table, counters, mode, st);
-  else launch_compress_rm<R, 1>(p, g, bitmap, table, counters, mode, st);
+  const int v = compress_variant();
+  if (v == 0) {
+    launch_compress_rm<R, 0>(p, g, bitmap, table, counters, mode, st);
+  } else if (v == 1) {
+    launch_compress_rm<R, 1>(p, g, bitmap, table, counters, mode, st);
+  } else {
+    if (mode == S2_MASK_GIVEN) launch_compress_tma<R, 2>(p, g, bitmap, table, counters, st);
+    else if (p.block_size == 1) launch_compress_tma<R, 0>(p, g, bitmap, table, counters, st);
+    else launch_compress_tma<R, 1>(p, g, bitmap, table, counters, st);
+  }
 }
 
 cudaError_t launch_compress(const Plan& p, const float* g, uint32_t* bitmap, float* table,
