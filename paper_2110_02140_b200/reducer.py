@@ -24,6 +24,20 @@ from .sketch import Plan
 from .sparse import DEFAULT_ROWS, DEFAULT_SIZE_RATIO, sketch_cols
 
 
+def broadcast_unique_id(rank: int, group=None) -> bytes:
+    """Rank 0 of ``group`` creates the NCCL unique id; every rank returns the same 128 bytes
+    (torch.distributed object broadcast; works over gloo or nccl)."""
+    import torch.distributed as dist
+
+    uid = (ctypes.c_uint8 * 128)()
+    if rank == 0:
+        check(lib.s2_nccl_unique_id(uid), "nccl unique id")
+    box = [bytes(uid)]
+    src = dist.get_global_rank(group, 0) if group is not None else 0
+    dist.broadcast_object_list(box, src=src, group=group)
+    return box[0]
+
+
 class S2Reducer:
     """Averaged sparse-sketch all-reduce of a flat float32 gradient.
 
@@ -52,12 +66,7 @@ class S2Reducer:
         self.world, self.rank = int(world), int(rank)
         uid = (ctypes.c_uint8 * 128)()
         if self.world > 1:
-            if self.rank == 0:
-                check(lib.s2_nccl_unique_id(uid), "nccl unique id")
-            box = [bytes(uid)]
-            dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0,
-                                       group=group)
-            ctypes.memmove(uid, box[0], 128)
+            ctypes.memmove(uid, broadcast_unique_id(self.rank, group), 128)
         check(lib.s2_comm_init(self.plan.handle, self.world, self.rank, uid), "comm init")
         check(lib.s2_comm_check(self.plan.handle, stream_ptr()), "comm check")
 

@@ -1,0 +1,31 @@
+"""Multi-GPU reduce (NCCL over NVLink) against the oracle; needs >= 2 GPUs (gpurun --gpus 2)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+
+def ngpus():
+    import torch
+
+    return torch.cuda.device_count()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_dist_reduce_parity(world):
+    if ngpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    port = 29500 + world
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "tools", "dist_check.py")]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    line = [x for x in p.stdout.splitlines() if x.startswith("{")][-1]
+    rep = json.loads(line)
+    assert rep["all_ranks_ok"], rep
