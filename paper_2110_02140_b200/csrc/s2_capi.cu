@@ -31,6 +31,12 @@ struct s2_plan {
   uint32_t* unionmap = nullptr;
   uint32_t* gather = nullptr;  // world * words (all-gather landing buffer)
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // optional phase timing events
+  // NVLink peer-memory exchange (world > 1, default): one IPC-shared arena per rank
+  bool p2p = false;
+  char* arena = nullptr;
+  char* peer[s2::kMaxWorld] = {};
+  s2::P2PArgs pa{};
+  int p2p_grid = 0;
 };
 
 namespace {
@@ -162,7 +168,7 @@ int s2_plan_create(int64_t dim, int64_t num_blocks, int rows, int64_t cols, uint
 
 static void free_scratch(s2_plan* p) {
   for (int k = 0; k < 2; ++k) {
-    cudaFree(p->tables[k]);
+    if (!p->p2p) cudaFree(p->tables[k]);
     cudaFree(p->counters[k]);
     p->tables[k] = nullptr;
     p->counters[k] = nullptr;
@@ -173,8 +179,21 @@ static void free_scratch(s2_plan* p) {
   p->bitmap = p->unionmap = p->gather = nullptr;
 }
 
+static void free_p2p(s2_plan* p) {
+  for (int q = 0; q < s2::kMaxWorld; ++q)
+    if (p->peer[q] && p->peer[q] != p->arena) cudaIpcCloseMemHandle(p->peer[q]);
+  for (int q = 0; q < s2::kMaxWorld; ++q) p->peer[q] = nullptr;
+  if (p->arena) cudaFree(p->arena);
+  p->arena = nullptr;
+  if (p->p2p) {  // tables/counters pointed into the arena / were separately allocated
+    p->tables[0] = p->tables[1] = nullptr;
+  }
+  p->p2p = false;
+}
+
 void s2_plan_destroy(s2_plan* plan) {
   if (!plan) return;
+  free_p2p(plan);
   if (plan->comm) ncclCommDestroy(plan->comm);
   free_scratch(plan);
   delete plan;
@@ -265,7 +284,7 @@ int s2_nccl_unique_id(void* out) {
 }
 
 static int ensure_scratch(s2_plan* p) {
-  if (p->tables[0]) return S2_OK;
+  if (p->tables[0] || p->p2p) return S2_OK;
   const size_t cells4 = ((size_t)p->p.hp.rows * p->p.hp.cols + 3) / 4 * 4;  // decode zeroes float4s
   const size_t wb = sizeof(uint32_t) * ((size_t)p->p.words + 4);
   for (int k = 0; k < 2; ++k) {
@@ -283,6 +302,88 @@ static int ensure_scratch(s2_plan* p) {
   return S2_OK;
 }
 
+static int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+// One cudaMalloc arena per rank, exported with CUDA IPC and mapped by every peer:
+//   tables[2] | bitmaps[2] | unions[2] | flags_a[W*G] | flags_b[W*G] | epochs[G]
+// The handles travel through one ncclAllGather.
+static int setup_p2p(s2_plan* plan) {
+  const int W = plan->world;
+  int dev = 0, sms = 0;
+  S2_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
+  S2_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sm count");
+  const int G = sms;
+  const int64_t cells = round_up((int64_t)plan->p.hp.rows * plan->p.hp.cols, 4 * W);
+  const int64_t words = round_up(plan->p.words, 4 * W);
+  s2::P2PArgs& a = plan->pa;
+  int64_t off = 0;
+  auto take = [&](int64_t bytes) {
+    const int64_t o = off;
+    off = round_up(off + bytes, 256);
+    return o;
+  };
+  for (int k = 0; k < 2; ++k) a.off_table[k] = take(cells * 4);
+  for (int k = 0; k < 2; ++k) a.off_bitmap[k] = take(words * 4);
+  for (int k = 0; k < 2; ++k) a.off_union[k] = take(words * 4);
+  a.off_flags_a = take((int64_t)W * G * 4);
+  a.off_flags_b = take((int64_t)W * G * 4);
+  a.off_epoch = take((int64_t)G * 4);
+  a.cells = cells;
+  a.words = words;
+  a.world = W;
+  a.rank = plan->rank;
+  S2_CUDA(cudaMalloc(&plan->arena, off), "cudaMalloc(arena)");
+  S2_CUDA(cudaMemset(plan->arena, 0, off), "cudaMemset(arena)");
+  S2_CUDA(cudaDeviceSynchronize(), "arena init");
+  struct Rec {
+    cudaIpcMemHandle_t h;
+    int64_t bytes;
+    int64_t grid;
+  } rec{};
+  S2_CUDA(cudaIpcGetMemHandle(&rec.h, plan->arena), "cudaIpcGetMemHandle");
+  rec.bytes = off;
+  rec.grid = G;
+  static_assert(sizeof(Rec) % 8 == 0, "rec");
+  char* d = nullptr;
+  S2_CUDA(cudaMalloc(&d, sizeof(Rec) * (W + 1)), "cudaMalloc(handles)");
+  std::vector<Rec> all(W);
+  cudaStream_t st = nullptr;
+  S2_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+  int rc = S2_OK;
+  if (cudaMemcpyAsync(d, &rec, sizeof rec, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      ncclAllGather(d, d + sizeof(Rec), sizeof(Rec), ncclUint8, plan->comm, st) != ncclSuccess ||
+      cudaMemcpyAsync(all.data(), d + sizeof(Rec), sizeof(Rec) * W, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    rc = fail(S2_ENCCL, "IPC handle exchange failed");
+  cudaFree(d);
+  cudaStreamDestroy(st);
+  if (rc) return rc;
+  for (int q = 0; q < W; ++q) {
+    if (all[q].bytes != off || all[q].grid != G)
+      return fail(S2_EINCOMPAT, "incompatible payloads: field 'sketch_params' differs (arena layout of rank %d)", q);
+    if (q == plan->rank) {
+      plan->peer[q] = plan->arena;
+    } else {
+      void* p = nullptr;
+      cudaError_t e = cudaIpcOpenMemHandle(&p, all[q].h, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle (set S2_AGG=nccl to use NCCL instead)");
+      plan->peer[q] = static_cast<char*>(p);
+    }
+    a.base[q] = plan->peer[q];
+  }
+  plan->p2p_grid = G;
+  plan->p2p = true;
+  // the ping-pong tables of s2_reduce live in the arena; counters stay private
+  for (int k = 0; k < 2; ++k) {
+    plan->tables[k] = reinterpret_cast<float*>(plan->arena + a.off_table[k]);
+    S2_CUDA(cudaMalloc(&plan->counters[k], sizeof(unsigned long long) * S2_NUM_COUNTERS), "cudaMalloc(counters)");
+    S2_CUDA(cudaMemset(plan->counters[k], 0, sizeof(unsigned long long) * S2_NUM_COUNTERS), "cudaMemset(counters)");
+  }
+  plan->phase = 0;
+  S2_CUDA(cudaDeviceSynchronize(), "p2p init");
+  return S2_OK;
+}
+
 int s2_comm_init(s2_plan* plan, int world, int rank, const void* unique_id) {
   if (!plan) return fail(S2_EINVAL, "NULL plan");
   if (world < 1 || rank < 0 || rank >= world) return fail(S2_EINVAL, "bad world/rank %d/%d", world, rank);
@@ -294,6 +395,12 @@ int s2_comm_init(s2_plan* plan, int world, int rank, const void* unique_id) {
     ncclUniqueId id;
     memcpy(&id, unique_id, sizeof id);
     S2_NCCL(ncclCommInitRank(&plan->comm, world, id, rank), "ncclCommInitRank");
+    const char* agg = getenv("S2_AGG");
+    if (!(agg && strcmp(agg, "nccl") == 0)) {
+      if (world > s2::kMaxWorld) return fail(S2_EINVAL, "peer-memory exchange supports world <= %d", s2::kMaxWorld);
+      int rc = setup_p2p(plan);
+      if (rc) return rc;
+    }
   }
   return ensure_scratch(plan);
 }
@@ -362,17 +469,24 @@ int s2_reduce(s2_plan* plan, const float* g, float* out, uint64_t* counters, voi
   cudaStream_t st = as_stream(stream);
   const int cur = plan->phase, nxt = cur ^ 1;
   float* table = plan->tables[cur];
+  uint32_t* bitmap = plan->p2p ? reinterpret_cast<uint32_t*>(plan->arena + plan->pa.off_bitmap[cur]) : plan->bitmap;
   // caller counters: zeroed by memset; plan counters: zeroed by the previous decode
   unsigned long long* cnt = counters ? reinterpret_cast<unsigned long long*>(counters) : plan->counters[cur];
   if (plan->ev[0]) cudaEventRecord(plan->ev[0], st);
-  S2_CUDA(s2::launch_compress(plan->p, g, plan->bitmap, table, cnt, S2_MASK_NONZERO, st, counters == nullptr),
+  S2_CUDA(s2::launch_compress(plan->p, g, bitmap, table, cnt, S2_MASK_NONZERO, st, counters == nullptr),
           "s2_reduce/compress");
   if (plan->ev[1]) cudaEventRecord(plan->ev[1], st);
-  const uint32_t* un = plan->bitmap;
+  const uint32_t* un = bitmap;
   if (plan->world > 1) {
-    rc = s2_aggregate(plan, table, plan->bitmap, plan->unionmap, stream);
-    if (rc) return rc;
-    un = plan->unionmap;
+    if (plan->p2p) {
+      plan->pa.cur = cur;
+      S2_CUDA(s2::launch_p2p_aggregate(plan->pa, plan->p2p_grid, st), "s2_reduce/p2p aggregate");
+      un = reinterpret_cast<const uint32_t*>(plan->arena + plan->pa.off_union[cur]);
+    } else {
+      rc = s2_aggregate(plan, table, bitmap, plan->unionmap, stream);
+      if (rc) return rc;
+      un = plan->unionmap;
+    }
   }
   if (plan->ev[2]) cudaEventRecord(plan->ev[2], st);
   S2_CUDA(s2::launch_decode(plan->p, un, table, plan->world, out, st, plan->tables[nxt], plan->counters[nxt]),

@@ -38,4 +38,16 @@ cudaError_t launch_compact(const Plan& p, const uint32_t* bitmap, const float* g
 cudaError_t launch_pairs(const Plan& p, const int64_t* idx, const float* vals, int64_t n, const float* table,
                          float* out, cudaStream_t st);
 
+// NVLink peer-memory exchange (s2_p2p.cu)
+constexpr int kMaxWorld = 8;
+struct P2PArgs {
+  char* base[kMaxWorld];  // arena base of every rank (self included), mapped in this process
+  int64_t off_table[2], off_bitmap[2], off_union[2];
+  int64_t off_flags_a, off_flags_b, off_epoch;
+  int64_t cells;  // table cells, padded to a multiple of 4 * world
+  int64_t words;  // bitmap words, padded to a multiple of 4 * world
+  int world, rank, cur;
+};
+cudaError_t launch_p2p_aggregate(const P2PArgs& a, int grid, cudaStream_t st);
+
 }  // namespace s2
