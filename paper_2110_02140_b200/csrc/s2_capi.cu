@@ -373,6 +373,12 @@ static int setup_p2p(s2_plan* plan) {
   }
   plan->p2p_grid = G;
   plan->p2p = true;
+  a.trace = nullptr;
+  const char* tr = getenv("S2_P2P_TRACE");
+  if (tr && atoi(tr)) {
+    S2_CUDA(cudaMalloc(&a.trace, sizeof(unsigned long long) * 8 * G), "cudaMalloc(trace)");
+    S2_CUDA(cudaMemset(a.trace, 0, sizeof(unsigned long long) * 8 * G), "cudaMemset(trace)");
+  }
   // the ping-pong tables of s2_reduce live in the arena; counters stay private
   for (int k = 0; k < 2; ++k) {
     plan->tables[k] = reinterpret_cast<float*>(plan->arena + a.off_table[k]);
@@ -493,6 +499,13 @@ int s2_reduce(s2_plan* plan, const float* g, float* out, uint64_t* counters, voi
           "s2_reduce/decode");
   if (plan->ev[3]) cudaEventRecord(plan->ev[3], st);
   plan->phase = nxt;
+  return S2_OK;
+}
+
+int s2_p2p_trace(const s2_plan* plan, uint64_t* host, int64_t n) {
+  if (!plan || !plan->p2p || !plan->pa.trace) return fail(S2_EINVAL, "no p2p trace (set S2_P2P_TRACE=1)");
+  const int64_t m = (int64_t)plan->p2p_grid * 8 < n ? (int64_t)plan->p2p_grid * 8 : n;
+  S2_CUDA(cudaMemcpy(host, plan->pa.trace, sizeof(uint64_t) * m, cudaMemcpyDeviceToHost), "trace copy");
   return S2_OK;
 }
 

@@ -47,6 +47,7 @@ struct P2PArgs {
   int64_t cells;  // table cells, padded to a multiple of 4 * world
   int64_t words;  // bitmap words, padded to a multiple of 4 * world
   int world, rank, cur;
+  unsigned long long* trace;  // optional: per-CTA globaltimer stamps [G][8] (S2_P2P_TRACE=1)
 };
 cudaError_t launch_p2p_aggregate(const P2PArgs& a, int grid, cudaStream_t st);
 

@@ -56,9 +56,22 @@ __device__ __forceinline__ void chunk_of(int64_t n, int64_t& lo, int64_t& hi) {
   if (lo > n) lo = n;
 }
 
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+#define S2_TRACE(slot)                                                          \
+  do {                                                                          \
+    if (a.trace != nullptr && threadIdx.x == 0)                                 \
+      a.trace[(int64_t)blockIdx.x * 8 + (slot)] = globaltimer();                \
+  } while (0)
+
 template <int W>
 __global__ void __launch_bounds__(512) k_p2p_aggregate(const __grid_constant__ P2PArgs a) {
   __shared__ uint32_t s_ep;
+  S2_TRACE(0);
   const int me = a.rank;
   const int cur = a.cur;
   if (threadIdx.x == 0) {
@@ -69,6 +82,7 @@ __global__ void __launch_bounds__(512) k_p2p_aggregate(const __grid_constant__ P
   __syncthreads();
   const uint32_t ep = s_ep;
   cross_rank_barrier<W>(a, a.off_flags_a, ep);
+  S2_TRACE(1);
 
   const int64_t t4 = a.cells / 4 / W;  // float4 per slice
   const int64_t w4 = a.words / 4 / W;  // uint4 per slice
@@ -108,7 +122,9 @@ __global__ void __launch_bounds__(512) k_p2p_aggregate(const __grid_constant__ P
       udst[i] = s;
     }
   }
+  S2_TRACE(2);
   cross_rank_barrier<W>(a, a.off_flags_b, ep);
+  S2_TRACE(3);
   {
     // phase B: every other rank's slice, chunk b
     int64_t lo, hi;
@@ -135,6 +151,8 @@ __global__ void __launch_bounds__(512) k_p2p_aggregate(const __grid_constant__ P
         if (q != me) udst[q * w4 + i] = v[q];
     }
   }
+  __syncthreads();
+  S2_TRACE(4);
 }
 
 cudaError_t launch_p2p_aggregate(const P2PArgs& a, int grid, cudaStream_t st) {
