@@ -35,10 +35,9 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
 
 template <int W>
 __device__ __forceinline__ void cross_rank_barrier(const P2PArgs& a, int64_t off_flags, uint32_t ep) {
-  __syncthreads();
+  __syncthreads();  // the CTA's writes happen-before thread q's release (bar.sync is cumulative)
   if (threadIdx.x < W) {
     const int q = threadIdx.x;
-    __threadfence_system();  // this CTA's phase writes before the flag (cumulative via bar.sync)
     uint32_t* remote = reinterpret_cast<uint32_t*>(a.base[q] + off_flags) + a.rank * gridDim.x + blockIdx.x;
     st_release_sys(remote, ep);
     const uint32_t* mine = reinterpret_cast<const uint32_t*>(a.base[a.rank] + off_flags) + q * gridDim.x + blockIdx.x;
@@ -68,89 +67,114 @@ __device__ __forceinline__ uint64_t globaltimer() {
       a.trace[(int64_t)blockIdx.x * 8 + (slot)] = globaltimer();                \
   } while (0)
 
+constexpr int kP2PThreads = 1024;
+// vectors per thread whose W loads are all in flight together (register budget: 64/thread)
 template <int W>
-__global__ void __launch_bounds__(512) k_p2p_aggregate(const __grid_constant__ P2PArgs a) {
+__host__ __device__ constexpr int p2p_batch() { return W <= 4 ? 2 : 1; }
+
+// One 16-byte vector v of the combined index space [table float4 | bitmap uint4]:
+// index i < t4 is table vector i, else bitmap vector i - t4 (per-slice indexing).
+template <int W>
+__device__ __forceinline__ void reduce_batch(const P2PArgs& a, int64_t i0, int64_t hi, int64_t t4, int64_t w4) {
+  const int me = a.rank, cur = a.cur;
+  constexpr int kP2PBatch = p2p_batch<W>();
+  uint4 v[kP2PBatch][W];
+#pragma unroll
+  for (int k = 0; k < kP2PBatch; ++k) {
+    const int64_t i = i0 + (int64_t)k * kP2PThreads;
+    if (i < hi) {
+      const bool tab = i < t4;
+      const int64_t off = tab ? a.off_table[cur] + (me * t4 + i) * 16 : a.off_bitmap[cur] + (me * w4 + i - t4) * 16;
+#pragma unroll
+      for (int q = 0; q < W; ++q) v[k][q] = __ldcg(reinterpret_cast<const uint4*>(a.base[q] + off));
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kP2PBatch; ++k) {
+    const int64_t i = i0 + (int64_t)k * kP2PThreads;
+    if (i < hi) {
+      uint4 s;
+      if (i < t4) {  // sketch.merge: fixed rank order 0..W-1 -> identical sums on every rank
+        float fx = __uint_as_float(v[k][0].x), fy = __uint_as_float(v[k][0].y);
+        float fz = __uint_as_float(v[k][0].z), fw = __uint_as_float(v[k][0].w);
+#pragma unroll
+        for (int q = 1; q < W; ++q) {
+          fx += __uint_as_float(v[k][q].x);
+          fy += __uint_as_float(v[k][q].y);
+          fz += __uint_as_float(v[k][q].z);
+          fw += __uint_as_float(v[k][q].w);
+        }
+        s = make_uint4(__float_as_uint(fx), __float_as_uint(fy), __float_as_uint(fz), __float_as_uint(fw));
+        *reinterpret_cast<uint4*>(a.base[me] + a.off_table[cur] + (me * t4 + i) * 16) = s;
+      } else {  // BlockMask.union
+        s = v[k][0];
+#pragma unroll
+        for (int q = 1; q < W; ++q) {
+          s.x |= v[k][q].x; s.y |= v[k][q].y; s.z |= v[k][q].z; s.w |= v[k][q].w;
+        }
+        *reinterpret_cast<uint4*>(a.base[me] + a.off_union[cur] + (me * w4 + i - t4) * 16) = s;
+      }
+    }
+  }
+}
+
+template <int W>
+__device__ __forceinline__ void gather_batch(const P2PArgs& a, int64_t i0, int64_t hi, int64_t t4, int64_t w4) {
+  const int me = a.rank, cur = a.cur;
+  constexpr int kP2PBatch = p2p_batch<W>();
+  uint4 v[kP2PBatch][W];
+#pragma unroll
+  for (int k = 0; k < kP2PBatch; ++k) {
+    const int64_t i = i0 + (int64_t)k * kP2PThreads;
+    if (i < hi) {
+      const bool tab = i < t4;
+#pragma unroll
+      for (int q = 0; q < W; ++q) {
+        if (q == me) continue;
+        const int64_t off = tab ? a.off_table[cur] + (q * t4 + i) * 16 : a.off_union[cur] + (q * w4 + i - t4) * 16;
+        v[k][q] = __ldcg(reinterpret_cast<const uint4*>(a.base[q] + off));
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kP2PBatch; ++k) {
+    const int64_t i = i0 + (int64_t)k * kP2PThreads;
+    if (i < hi) {
+      const bool tab = i < t4;
+#pragma unroll
+      for (int q = 0; q < W; ++q) {
+        if (q == me) continue;
+        const int64_t off = tab ? a.off_table[cur] + (q * t4 + i) * 16 : a.off_union[cur] + (q * w4 + i - t4) * 16;
+        *reinterpret_cast<uint4*>(a.base[me] + off) = v[k][q];
+      }
+    }
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(kP2PThreads) k_p2p_aggregate(const __grid_constant__ P2PArgs a) {
   __shared__ uint32_t s_ep;
   S2_TRACE(0);
-  const int me = a.rank;
-  const int cur = a.cur;
   if (threadIdx.x == 0) {
-    uint32_t* e = reinterpret_cast<uint32_t*>(a.base[me] + a.off_epoch) + blockIdx.x;
+    uint32_t* e = reinterpret_cast<uint32_t*>(a.base[a.rank] + a.off_epoch) + blockIdx.x;
     s_ep = *e + 1u;
     *e = s_ep;
   }
   __syncthreads();
   const uint32_t ep = s_ep;
+  const int64_t t4 = a.cells / 4 / W;  // 16-byte vectors per slice: table ...
+  const int64_t w4 = a.words / 4 / W;  // ... and bitmap
+  int64_t lo, hi;
+  chunk_of(t4 + w4, lo, hi);
   cross_rank_barrier<W>(a, a.off_flags_a, ep);
   S2_TRACE(1);
-
-  const int64_t t4 = a.cells / 4 / W;  // float4 per slice
-  const int64_t w4 = a.words / 4 / W;  // uint4 per slice
-  {
-    // phase A: slice `me`
-    int64_t lo, hi;
-    chunk_of(t4, lo, hi);
-    const float4* src[W];
-#pragma unroll
-    for (int q = 0; q < W; ++q) src[q] = reinterpret_cast<const float4*>(a.base[q] + a.off_table[cur]) + me * t4;
-    float4* dst = reinterpret_cast<float4*>(a.base[me] + a.off_table[cur]) + me * t4;
-    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-      float4 v[W];
-#pragma unroll
-      for (int q = 0; q < W; ++q) v[q] = __ldcg(src[q] + i);
-      float4 s = v[0];
-#pragma unroll
-      for (int q = 1; q < W; ++q) {
-        s.x += v[q].x; s.y += v[q].y; s.z += v[q].z; s.w += v[q].w;
-      }
-      dst[i] = s;
-    }
-    chunk_of(w4, lo, hi);
-    const uint4* bsrc[W];
-#pragma unroll
-    for (int q = 0; q < W; ++q) bsrc[q] = reinterpret_cast<const uint4*>(a.base[q] + a.off_bitmap[cur]) + me * w4;
-    uint4* udst = reinterpret_cast<uint4*>(a.base[me] + a.off_union[cur]) + me * w4;
-    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-      uint4 v[W];
-#pragma unroll
-      for (int q = 0; q < W; ++q) v[q] = __ldcg(bsrc[q] + i);
-      uint4 s = v[0];
-#pragma unroll
-      for (int q = 1; q < W; ++q) {
-        s.x |= v[q].x; s.y |= v[q].y; s.z |= v[q].z; s.w |= v[q].w;
-      }
-      udst[i] = s;
-    }
-  }
+  for (int64_t i0 = lo + threadIdx.x; i0 < hi; i0 += (int64_t)p2p_batch<W>() * kP2PThreads)
+    reduce_batch<W>(a, i0, hi, t4, w4);  // phase A: reduce-scatter
   S2_TRACE(2);
   cross_rank_barrier<W>(a, a.off_flags_b, ep);
   S2_TRACE(3);
-  {
-    // phase B: every other rank's slice, chunk b
-    int64_t lo, hi;
-    chunk_of(t4, lo, hi);
-    float4* tdst = reinterpret_cast<float4*>(a.base[me] + a.off_table[cur]);
-    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-      float4 v[W];
-#pragma unroll
-      for (int q = 0; q < W; ++q)
-        if (q != me) v[q] = __ldcg(reinterpret_cast<const float4*>(a.base[q] + a.off_table[cur]) + q * t4 + i);
-#pragma unroll
-      for (int q = 0; q < W; ++q)
-        if (q != me) tdst[q * t4 + i] = v[q];
-    }
-    chunk_of(w4, lo, hi);
-    uint4* udst = reinterpret_cast<uint4*>(a.base[me] + a.off_union[cur]);
-    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-      uint4 v[W];
-#pragma unroll
-      for (int q = 0; q < W; ++q)
-        if (q != me) v[q] = __ldcg(reinterpret_cast<const uint4*>(a.base[q] + a.off_union[cur]) + q * w4 + i);
-#pragma unroll
-      for (int q = 0; q < W; ++q)
-        if (q != me) udst[q * w4 + i] = v[q];
-    }
-  }
+  for (int64_t i0 = lo + threadIdx.x; i0 < hi; i0 += (int64_t)p2p_batch<W>() * kP2PThreads)
+    gather_batch<W>(a, i0, hi, t4, w4);  // phase B: all-gather
   __syncthreads();
   S2_TRACE(4);
 }
@@ -168,7 +192,7 @@ cudaError_t launch_p2p_aggregate(const P2PArgs& a, int grid, cudaStream_t st) {
     case 8: fn = (const void*)k_p2p_aggregate<8>; break;
     default: return cudaErrorInvalidValue;
   }
-  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(512), args, 0, st);
+  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kP2PThreads), args, 0, st);
 }
 
 }  // namespace s2
