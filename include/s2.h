@@ -138,6 +138,8 @@ const uint64_t* s2_last_counters(const s2_plan* plan);
 /* optional: 4 caller-created cudaEvent_t that s2_reduce records before compress,
  * after compress, after aggregate and after decode (n = 0 disables) */
 int s2_plan_set_timing_events(s2_plan* plan, void* const* events, int n);
+/* != 0 if a peer-memory barrier gave up after 10 s (a rank died or diverged); syncs */
+int s2_p2p_error(const s2_plan* plan);
 /* debugging: globaltimer stamps [G][8] of the last peer-memory exchange (S2_P2P_TRACE=1) */
 int s2_p2p_trace(const s2_plan* plan, uint64_t* host, int64_t n);
 /* copy those counters to host (synchronises `stream`) */

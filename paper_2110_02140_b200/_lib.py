@@ -60,6 +60,7 @@ SIGNATURES = {
     "s2_read_counters": (c_int, [c_void_p, c_void_p, c_void_p]),
     "s2_plan_set_timing_events": (c_int, [c_void_p, c_void_p, c_int]),
     "s2_p2p_trace": (c_int, [c_void_p, c_void_p, c_int64]),
+    "s2_p2p_error": (c_int, [c_void_p]),
 }
 
 

@@ -328,6 +328,11 @@ static int setup_p2p(s2_plan* plan) {
   a.off_flags_a = take((int64_t)W * G * 4);
   a.off_flags_b = take((int64_t)W * G * 4);
   a.off_epoch = take((int64_t)G * 4);
+  a.off_error = take(256);
+  const char* os_env = getenv("S2_P2P_ONESHOT_MAXW");
+  const int oneshot_maxw = os_env ? atoi(os_env) : 2;
+  a.oneshot = (W <= oneshot_maxw && W <= 4) ? 1 : 0;
+  for (int k = 0; k < 2; ++k) a.off_tsum[k] = a.oneshot ? take(cells * 4) : a.off_table[k];
   a.cells = cells;
   a.words = words;
   a.world = W;
@@ -488,6 +493,7 @@ int s2_reduce(s2_plan* plan, const float* g, float* out, uint64_t* counters, voi
       plan->pa.cur = cur;
       S2_CUDA(s2::launch_p2p_aggregate(plan->pa, plan->p2p_grid, st), "s2_reduce/p2p aggregate");
       un = reinterpret_cast<const uint32_t*>(plan->arena + plan->pa.off_union[cur]);
+      table = reinterpret_cast<float*>(plan->arena + plan->pa.off_tsum[cur]);  // == tables[cur] when two-shot
     } else {
       rc = s2_aggregate(plan, table, bitmap, plan->unionmap, stream);
       if (rc) return rc;
@@ -500,6 +506,13 @@ int s2_reduce(s2_plan* plan, const float* g, float* out, uint64_t* counters, voi
   if (plan->ev[3]) cudaEventRecord(plan->ev[3], st);
   plan->phase = nxt;
   return S2_OK;
+}
+
+int s2_p2p_error(const s2_plan* plan) {
+  if (!plan || !plan->p2p) return 0;
+  uint32_t e = 0;
+  cudaMemcpy(&e, plan->arena + plan->pa.off_error, 4, cudaMemcpyDeviceToHost);
+  return (int)e;
 }
 
 int s2_p2p_trace(const s2_plan* plan, uint64_t* host, int64_t n) {

@@ -43,10 +43,12 @@ constexpr int kMaxWorld = 8;
 struct P2PArgs {
   char* base[kMaxWorld];  // arena base of every rank (self included), mapped in this process
   int64_t off_table[2], off_bitmap[2], off_union[2];
-  int64_t off_flags_a, off_flags_b, off_epoch;
+  int64_t off_flags_a, off_flags_b, off_epoch, off_error;
+  int64_t off_tsum[2];  // one-shot: private summed tables
   int64_t cells;  // table cells, padded to a multiple of 4 * world
   int64_t words;  // bitmap words, padded to a multiple of 4 * world
   int world, rank, cur;
+  int oneshot;                // 1: one-shot exchange (single barrier), 0: two-shot
   unsigned long long* trace;  // optional: per-CTA globaltimer stamps [G][8] (S2_P2P_TRACE=1)
 };
 cudaError_t launch_p2p_aggregate(const P2PArgs& a, int grid, cudaStream_t st);

@@ -33,6 +33,10 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   return v;
 }
 
+__device__ __forceinline__ uint64_t globaltimer();
+
+// CTA b of this rank <-> CTA b of every rank.  A spin that outlives 10 s records an error
+// in the arena and gives up instead of hanging the GPU (a peer died or diverged).
 template <int W>
 __device__ __forceinline__ void cross_rank_barrier(const P2PArgs& a, int64_t off_flags, uint32_t ep) {
   __syncthreads();  // the CTA's writes happen-before thread q's release (bar.sync is cumulative)
@@ -41,7 +45,16 @@ __device__ __forceinline__ void cross_rank_barrier(const P2PArgs& a, int64_t off
     uint32_t* remote = reinterpret_cast<uint32_t*>(a.base[q] + off_flags) + a.rank * gridDim.x + blockIdx.x;
     st_release_sys(remote, ep);
     const uint32_t* mine = reinterpret_cast<const uint32_t*>(a.base[a.rank] + off_flags) + q * gridDim.x + blockIdx.x;
-    while ((int32_t)(ld_acquire_sys(mine) - ep) < 0) {
+    uint64_t t0 = 0;
+    for (int spin = 0; (int32_t)(ld_acquire_sys(mine) - ep) < 0; ++spin) {
+      if ((spin & 1023) == 1023) {
+        const uint64_t now = globaltimer();
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > 10000000000ull) {
+          atomicOr(reinterpret_cast<uint32_t*>(a.base[a.rank] + a.off_error), 1u);
+          break;
+        }
+      }
     }
   }
   __syncthreads();
@@ -179,7 +192,79 @@ __global__ void __launch_bounds__(kP2PThreads) k_p2p_aggregate(const __grid_cons
   S2_TRACE(4);
 }
 
+// One-shot variant (small W): after barrier 1 every rank reduces the WHOLE table and bitmap
+// from all W ranks into private buffers (sum -> tsum[cur], OR -> union[cur]); one barrier,
+// (W-1) x (table + bitmap) bytes over NVLink per rank.
+template <int W>
+__global__ void __launch_bounds__(kP2PThreads) k_p2p_oneshot(const __grid_constant__ P2PArgs a) {
+  __shared__ uint32_t s_ep;
+  S2_TRACE(0);
+  if (threadIdx.x == 0) {
+    uint32_t* e = reinterpret_cast<uint32_t*>(a.base[a.rank] + a.off_epoch) + blockIdx.x;
+    s_ep = *e + 1u;
+    *e = s_ep;
+  }
+  __syncthreads();
+  const int me = a.rank, cur = a.cur;
+  const int64_t t4 = a.cells / 4, w4 = a.words / 4;
+  int64_t lo, hi;
+  chunk_of(t4 + w4, lo, hi);
+  cross_rank_barrier<W>(a, a.off_flags_a, s_ep);
+  S2_TRACE(1);
+  constexpr int B = p2p_batch<W>();
+  for (int64_t i0 = lo + threadIdx.x; i0 < hi; i0 += (int64_t)B * kP2PThreads) {
+    uint4 v[B][W];
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      const int64_t i = i0 + (int64_t)k * kP2PThreads;
+      if (i < hi) {
+        const int64_t off = i < t4 ? a.off_table[cur] + i * 16 : a.off_bitmap[cur] + (i - t4) * 16;
+#pragma unroll
+        for (int q = 0; q < W; ++q) v[k][q] = __ldcg(reinterpret_cast<const uint4*>(a.base[q] + off));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      const int64_t i = i0 + (int64_t)k * kP2PThreads;
+      if (i >= hi) continue;
+      if (i < t4) {
+        float fx = __uint_as_float(v[k][0].x), fy = __uint_as_float(v[k][0].y);
+        float fz = __uint_as_float(v[k][0].z), fw = __uint_as_float(v[k][0].w);
+#pragma unroll
+        for (int q = 1; q < W; ++q) {
+          fx += __uint_as_float(v[k][q].x);
+          fy += __uint_as_float(v[k][q].y);
+          fz += __uint_as_float(v[k][q].z);
+          fw += __uint_as_float(v[k][q].w);
+        }
+        *reinterpret_cast<uint4*>(a.base[me] + a.off_tsum[cur] + i * 16) =
+            make_uint4(__float_as_uint(fx), __float_as_uint(fy), __float_as_uint(fz), __float_as_uint(fw));
+      } else {
+        uint4 o = v[k][0];
+#pragma unroll
+        for (int q = 1; q < W; ++q) {
+          o.x |= v[k][q].x; o.y |= v[k][q].y; o.z |= v[k][q].z; o.w |= v[k][q].w;
+        }
+        *reinterpret_cast<uint4*>(a.base[me] + a.off_union[cur] + (i - t4) * 16) = o;
+      }
+    }
+  }
+  __syncthreads();
+  S2_TRACE(4);
+}
+
 cudaError_t launch_p2p_aggregate(const P2PArgs& a, int grid, cudaStream_t st) {
+  if (a.oneshot) {
+    void* args[] = {const_cast<P2PArgs*>(&a)};
+    const void* fn = nullptr;
+    switch (a.world) {
+      case 2: fn = (const void*)k_p2p_oneshot<2>; break;
+      case 3: fn = (const void*)k_p2p_oneshot<3>; break;
+      case 4: fn = (const void*)k_p2p_oneshot<4>; break;
+      default: return cudaErrorInvalidValue;
+    }
+    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kP2PThreads), args, 0, st);
+  }
   void* args[] = {const_cast<P2PArgs*>(&a)};
   const void* fn = nullptr;
   switch (a.world) {
