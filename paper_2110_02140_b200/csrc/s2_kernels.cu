@@ -881,13 +881,14 @@ static int grid_for(int64_t ntiles, int ctas_per_sm) {
   return gr < 1 ? 1 : (int)gr;
 }
 
-// S2_COMPRESS_LOAD: 0 register prefetch | 1 TMA, coalesced layout | 2 TMA-staged, swizzled (default)
+// S2_COMPRESS_LOAD: 0 register prefetch (default: fastest measured, profiles/r01_*) |
+//                   1 TMA prefetch, coalesced layout | 2 TMA-staged 2-stage ring, swizzled
 static int compress_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("S2_COMPRESS_LOAD");
-    v = e ? atoi(e) : 2;
-    if (v < 0 || v > 2) v = 2;
+    v = e ? atoi(e) : 0;
+    if (v < 0 || v > 2) v = 0;
   }
   return v;
 }
