@@ -95,3 +95,57 @@ class S2Reducer:
 
     def last_nnz(self) -> int:
         return self.counters()[S2_CNT_NNZ]
+
+
+class HostPipeline:
+    """Reduce gradients that live in (pinned) host memory, overlapping PCIe with the GPU.
+
+    ``submit(g_host, out_host)`` enqueues H2D of the gradient on a copy-in stream,
+    the reduce on the compute stream and D2H of the result on a copy-out stream,
+    with double-buffered device staging, so step i's reduce overlaps step i+1's
+    H2D and step i-1's D2H (PCIe is full duplex).  It returns a CUDA event that
+    completes when ``out_host`` holds the result; ``drain()`` waits for all.
+    """
+
+    def __init__(self, reducer: S2Reducer, depth: int = 2):
+        self.r = reducer
+        dev = reducer.device
+        self.depth = depth
+        self.s_in = torch.cuda.Stream(device=dev)
+        self.s_comp = torch.cuda.Stream(device=dev)
+        self.s_out = torch.cuda.Stream(device=dev)
+        self.g = [torch.empty(reducer.dim, dtype=torch.float32, device=dev) for _ in range(depth)]
+        self.o = [torch.empty(reducer.dim, dtype=torch.float32, device=dev) for _ in range(depth)]
+        self.comp_done = [None] * depth  # reduce i finished reading g[i%depth] / writing o[i%depth]
+        self.out_done = [None] * depth   # D2H of o[i%depth] finished
+        self.i = 0
+
+    def submit(self, g_host: torch.Tensor, out_host: torch.Tensor) -> torch.cuda.Event:
+        k = self.i % self.depth
+        self.i += 1
+        with torch.cuda.stream(self.s_in):
+            if self.comp_done[k] is not None:
+                self.s_in.wait_event(self.comp_done[k])  # g[k] free again
+            self.g[k].copy_(g_host, non_blocking=True)
+            in_done = torch.cuda.Event()
+            in_done.record(self.s_in)
+        with torch.cuda.stream(self.s_comp):
+            self.s_comp.wait_event(in_done)
+            if self.out_done[k] is not None:
+                self.s_comp.wait_event(self.out_done[k])  # o[k] drained to the host
+            self.r.reduce(self.g[k], out=self.o[k], stream=self.s_comp)
+            ev = torch.cuda.Event()
+            ev.record(self.s_comp)
+            self.comp_done[k] = ev
+        with torch.cuda.stream(self.s_out):
+            self.s_out.wait_event(ev)
+            out_host.copy_(self.o[k], non_blocking=True)
+            od = torch.cuda.Event()
+            od.record(self.s_out)
+            self.out_done[k] = od
+        return od
+
+    def drain(self) -> None:
+        for e in self.out_done:
+            if e is not None:
+                e.synchronize()

@@ -322,3 +322,23 @@ def test_compressor_plugin_nonzero(s2):
     ref = o.decompress(o.compress(g, g != 0, 3, comp.cols, 0))
     assert np.array_equal(host(est), ref.astype(np.float32))
     assert comp.payload_nbytes(pay) == 53 + (d + 7) // 8 + 4 * 3 * comp.cols
+
+
+def test_host_pipeline(s2):
+    """HostPipeline: pinned host gradients in, host results out, copies overlapped across steps."""
+    import torch
+
+    from paper_2110_02140_b200.reducer import HostPipeline
+
+    d = 1_000_003
+    red = s2.S2Reducer(d, rows=3, cols=7919, seed=3)
+    pipe = HostPipeline(red)
+    gs = [o.synthetic_gradient(d, a, k, kind="int") for k, a in enumerate((0.01, 0.03, 0.002, 0.01, 0.05))]
+    hin = [torch.from_numpy(g).pin_memory() for g in gs]
+    hout = [torch.empty(d, dtype=torch.float32).pin_memory() for _ in gs]
+    for gi, go in zip(hin, hout):
+        pipe.submit(gi, go)
+    pipe.drain()
+    for g, go in zip(gs, hout):
+        ref = o.decompress(o.compress(g, g != 0, 3, 7919, 3))
+        assert np.array_equal(go.numpy(), ref.astype(np.float32))
