@@ -170,7 +170,7 @@ k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __res
   constexpr int kCap = 32 + kQFast;
   __shared__ uint32_t s_qi[kWarps][kCap];
   __shared__ float s_qv[kWarps][kCap];
-  __shared__ __align__(128) float4 s_tile[LOAD == 1 ? kWarps : 1][kTile / 4];
+  __shared__ __align__(128) float4 s_tile[kWarps][kTile / 4];  // LOAD 1: TMA target; LOAD 0: value stage
   __shared__ __align__(8) uint64_t s_bar[kWarps];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -274,16 +274,34 @@ k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __res
       nnz += (unsigned)total;
       if (qn + total <= kCap) {
         int pos = qn + incl - cnt;
-        const uint32_t e0 = (uint32_t)(base + lane * 4);
+        if (LOAD == 0) {
+          // stage the tile (8 STS.128 per lane) so the append loop can index values dynamically:
+          // ~popc(m) iterations instead of 32 per-element predicated appends
+          float4* st = s_tile[wib];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t nib = (m >> (4 * k)) & 0xFu;
-          if (nib) {
-            const uint32_t e = e0 + 128u * k;
-            if (nib & 1u) { qi[pos] = e + 0; qv[pos] = v[k].x; ++pos; }
-            if (nib & 2u) { qi[pos] = e + 1; qv[pos] = v[k].y; ++pos; }
-            if (nib & 4u) { qi[pos] = e + 2; qv[pos] = v[k].z; ++pos; }
-            if (nib & 8u) { qi[pos] = e + 3; qv[pos] = v[k].w; ++pos; }
+          for (int k = 0; k < 8; ++k) st[k * 32 + lane] = v[k];
+          __syncwarp();
+          const float* sf = reinterpret_cast<const float*>(st);
+          for (uint32_t mm = m; mm; mm &= mm - 1u) {
+            const int b = __ffs(mm) - 1;  // bit 4k+c <-> tile offset 128k + 4*lane + c
+            const uint32_t off = 128u * (uint32_t)(b >> 2) + 4u * lane + (uint32_t)(b & 3);
+            qi[pos] = (uint32_t)base + off;
+            qv[pos] = sf[off];
+            ++pos;
+          }
+          __syncwarp();
+        } else {
+          const uint32_t e0 = (uint32_t)(base + lane * 4);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint32_t nib = (m >> (4 * k)) & 0xFu;
+            if (nib) {
+              const uint32_t e = e0 + 128u * k;
+              if (nib & 1u) { qi[pos] = e + 0; qv[pos] = v[k].x; ++pos; }
+              if (nib & 2u) { qi[pos] = e + 1; qv[pos] = v[k].y; ++pos; }
+              if (nib & 4u) { qi[pos] = e + 2; qv[pos] = v[k].z; ++pos; }
+              if (nib & 8u) { qi[pos] = e + 3; qv[pos] = v[k].w; ++pos; }
+            }
           }
         }
         qn += total;

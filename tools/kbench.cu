@@ -84,3 +84,69 @@ extern "C" int kb_write(float* o, int64_t n, int stream_hint, int grid, void* st
   else k_write<false><<<grid, 256, 0, s>>>(o, n);
   return (int)cudaGetLastError();
 }
+
+// ---- TMA streaming read: per-warp ring of STAGES x TILE-byte bulk copies ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+                   "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile("{\n\t.reg .pred p;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n}" ::
+                   "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+template <int STAGES, int TILEB>
+__global__ void k_tma_read(const float* __restrict__ g, int64_t n, uint32_t* __restrict__ out) {
+  extern __shared__ __align__(128) unsigned char s_raw[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  unsigned char* ring = s_raw + (size_t)wib * STAGES * TILEB;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_raw + (size_t)nwarps * STAGES * TILEB) + wib * STAGES;
+  const int64_t ntiles = n * 4 / TILEB;
+  const int64_t nw = (int64_t)gridDim.x * nwarps;
+  int64_t t = (int64_t)blockIdx.x * nwarps + wib;
+  if (lane == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < STAGES; ++s)
+      if (t + s * nw < ntiles) tma_load_1d(ring + s * TILEB, (const char*)g + (t + s * nw) * TILEB, TILEB, &bars[s]);
+  }
+  __syncwarp();
+  uint32_t acc = 0, parity = 0;
+  int stage = 0;
+  for (; t < ntiles; t += nw) {
+    mbar_wait(&bars[stage], (parity >> stage) & 1u);
+    parity ^= 1u << stage;
+    const float4* tile = reinterpret_cast<const float4*>(ring + stage * TILEB);
+#pragma unroll 4
+    for (int k = lane; k < TILEB / 16; k += 32) {
+      const float4 x = tile[k];
+      acc ^= __float_as_uint(x.x) ^ __float_as_uint(x.w);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0 && t + STAGES * nw < ntiles)
+      tma_load_1d(ring + stage * TILEB, (const char*)g + (t + STAGES * nw) * TILEB, TILEB, &bars[stage]);
+    stage = stage + 1 == STAGES ? 0 : stage + 1;
+  }
+  if (acc == 0x12345678u) out[0] = acc;
+}
+
+extern "C" int kb_tma_read(const float* g, int64_t n, uint32_t* out, int stages, int tileb, int warps, int ctas_per_sm,
+                           int sms, void* st) {
+  const int smem = warps * stages * tileb + warps * stages * 8;
+  cudaStream_t s = (cudaStream_t)st;
+  const void* fn = nullptr;
+#define C(S, T) if (stages == S && tileb == T) fn = (const void*)k_tma_read<S, T>;
+  C(2, 4096) C(3, 4096) C(4, 4096) C(2, 8192) C(3, 8192) C(2, 16384) C(4, 2048) C(8, 2048)
+#undef C
+  if (!fn) return -1;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  void* args[] = {&g, &n, &out};
+  cudaError_t e = cudaLaunchKernel(fn, dim3(sms * ctas_per_sm), dim3(warps * 32), args, smem, s);
+  return (int)e;
+}
