@@ -21,6 +21,7 @@
 // bitmap words = 8 float4 per lane.
 #include <cstdio>
 #include <cstdlib>
+#include <utility>
 
 #include "s2_common.cuh"
 #include "s2_kernels.h"
@@ -40,6 +41,41 @@ static int num_sms() {
     if (g_num_sms <= 0) g_num_sms = 148;
   }
   return g_num_sms;
+}
+
+// --------------------------------------------------- programmatic dependent launch
+// k_compress / k_decode are launched with programmatic stream serialization: their CTAs
+// become resident while the previous kernel drains, and griddepcontrol.wait holds them
+// until that kernel's memory is visible.  Work that touches nothing the predecessor
+// writes (the decode's zeroing of the NEXT ping-pong table) runs before the wait.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+static bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("S2_PDL");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                             Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 // ------------------------------------------------------------------ insert
@@ -189,6 +225,8 @@ k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __res
   uint32_t bad = 0;
   float fin = 0.f;  // MODE 2: sum of 0*x, NaN iff a non-finite element was seen
 
+  griddep_wait();  // g may be written by the caller's previous kernel
+  griddep_launch_dependents();
   int64_t t = (int64_t)blockIdx.x * kWarps + wib;
   float4 vn[LOAD == 0 ? 8 : 1];
   uint32_t parity = 0;
@@ -402,6 +440,8 @@ k_compress_tma(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* _
   const int64_t nelem_words = (dim + 31) / 32;
   const int64_t nw = (int64_t)gridDim.x * kTWarps;
   const uint64_t pol = policy_evict_first();
+  griddep_wait();
+  griddep_launch_dependents();
 
   if (lane == 0) {
     for (int s = 0; s < kTStages; ++s) mbar_init(&bars[s], 1);
@@ -618,6 +658,8 @@ k_decode(const uint32_t* __restrict__ bitmap, int64_t dim, int64_t bs,
       zt[i] = z;
   }
   if (zc != nullptr && blockIdx.x == 0 && threadIdx.x < S2_NUM_COUNTERS) zc[threadIdx.x] = 0ull;
+  griddep_wait();  // bitmap + table come from the compress / exchange kernel
+  griddep_launch_dependents();
   __shared__ uint16_t s_q[kWarps][kTile];
   __shared__ __align__(16) float s_v[kWarps][kTile];
   const int lane = threadIdx.x & 31;
@@ -917,11 +959,11 @@ static void launch_compress_rm(const Plan& p, const float* g, uint32_t* bitmap, 
   const int64_t ntiles = (p.dim + kTile - 1) / kTile;
   const int grid = grid_for(ntiles, LOAD == 0 ? 2 : 4);
   if (mode == S2_MASK_GIVEN) {
-    k_compress<R, 2, LOAD><<<grid, kThreads, 0, st>>>(g, p.dim, p.block_size, bitmap, table, counters, p.hp);
+    launch_ex(k_compress<R, 2, LOAD>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table, counters, p.hp);
   } else if (p.block_size == 1) {
-    k_compress<R, 0, LOAD><<<grid, kThreads, 0, st>>>(g, p.dim, p.block_size, bitmap, table, counters, p.hp);
+    launch_ex(k_compress<R, 0, LOAD>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table, counters, p.hp);
   } else {
-    k_compress<R, 1, LOAD><<<grid, kThreads, 0, st>>>(g, p.dim, p.block_size, bitmap, table, counters, p.hp);
+    launch_ex(k_compress<R, 1, LOAD>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table, counters, p.hp);
   }
 }
 
@@ -937,8 +979,8 @@ static void launch_compress_tma(const Plan& p, const float* g, uint32_t* bitmap,
   int64_t grid = (ntiles + kTWarps - 1) / kTWarps;
   const int64_t cap = (int64_t)num_sms() * 5;
   if (grid > cap) grid = cap;
-  k_compress_tma<R, MODE><<<(int)grid, kTWarps * 32, kTSmemBytes, st>>>(g, p.dim, p.block_size, bitmap, table,
-                                                                        counters, p.hp);
+  launch_ex(k_compress_tma<R, MODE>, (int)grid, kTWarps * 32, kTSmemBytes, st, g, p.dim, p.block_size, bitmap,
+            table, counters, p.hp);
 }
 
 template <int R>
@@ -993,11 +1035,11 @@ static void launch_decode_r(const Plan& p, const uint32_t* bitmap, const float* 
   const int64_t zn4 = zt ? ((int64_t)p.hp.rows * p.hp.cols + 3) / 4 : 0;
   float4* z4 = reinterpret_cast<float4*>(zt);
   if (p.block_size == 1)
-    k_decode<R, false><<<grid, kThreads, 0, st>>>(bitmap, p.dim, 1, table, (float)workers, inv, pow2, out, z4,
-                                                  zn4, zc, p.hp);
+    launch_ex(k_decode<R, false>, grid, kThreads, 0, st, bitmap, p.dim, (int64_t)1, table, (float)workers, inv, pow2,
+              out, z4, zn4, zc, p.hp);
   else
-    k_decode<R, true><<<grid, kThreads, 0, st>>>(bitmap, p.dim, p.block_size, table, (float)workers, inv, pow2,
-                                                 out, z4, zn4, zc, p.hp);
+    launch_ex(k_decode<R, true>, grid, kThreads, 0, st, bitmap, p.dim, p.block_size, table, (float)workers, inv,
+              pow2, out, z4, zn4, zc, p.hp);
 }
 
 cudaError_t launch_decode(const Plan& p, const uint32_t* bitmap, const float* table, int workers,
