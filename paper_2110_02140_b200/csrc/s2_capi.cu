@@ -332,6 +332,11 @@ static int setup_p2p(s2_plan* plan) {
   const char* os_env = getenv("S2_P2P_ONESHOT_MAXW");
   const int oneshot_maxw = os_env ? atoi(os_env) : 2;
   a.oneshot = (W <= oneshot_maxw && W <= 4) ? 1 : 0;
+  // W <= 4: the decode ORs the W bitmaps straight from peer memory, the exchange moves only the
+  // table; above that the OR is reduce-scattered with the table (less NVLink traffic per rank)
+  const char* bd_env = getenv("S2_P2P_BITMAP_IN_DECODE_MAXW");
+  const int bd_maxw = bd_env ? atoi(bd_env) : 4;
+  a.table_only = (W <= bd_maxw && plan->p.block_size == 1) ? 1 : 0;
   for (int k = 0; k < 2; ++k) a.off_tsum[k] = a.oneshot ? take(cells * 4) : a.off_table[k];
   a.cells = cells;
   a.words = words;
@@ -501,7 +506,14 @@ int s2_reduce(s2_plan* plan, const float* g, float* out, uint64_t* counters, voi
     }
   }
   if (plan->ev[2]) cudaEventRecord(plan->ev[2], st);
-  S2_CUDA(s2::launch_decode(plan->p, un, table, plan->world, out, st, plan->tables[nxt], plan->counters[nxt]),
+  s2::PeerMaps pm{};
+  if (plan->p2p && plan->pa.table_only) {
+    pm.n = plan->world;
+    for (int q = 0; q < plan->world; ++q)
+      pm.p[q] = reinterpret_cast<const uint32_t*>(plan->pa.base[q] + plan->pa.off_bitmap[cur]);
+  }
+  S2_CUDA(s2::launch_decode(plan->p, un, table, plan->world, out, st, plan->tables[nxt], plan->counters[nxt],
+                            pm.n ? &pm : nullptr),
           "s2_reduce/decode");
   if (plan->ev[3]) cudaEventRecord(plan->ev[3], st);
   plan->phase = nxt;

@@ -631,12 +631,23 @@ __device__ __forceinline__ float query_one(uint64_t i, const float* __restrict__
 }
 
 template <bool BLOCKS>
-__device__ __forceinline__ uint32_t decode_word(const uint32_t* __restrict__ bitmap, int64_t t, int lane,
-                                               int64_t dim, int64_t bs, int64_t nelem_words) {
+__device__ __forceinline__ uint32_t decode_word(const uint32_t* __restrict__ bitmap, const PeerMaps& pm, int64_t t,
+                                               int lane, int64_t dim, int64_t bs, int64_t nelem_words) {
   const int64_t e0 = t * kTile + 32 * lane;
-  uint32_t word;
+  uint32_t word = 0;
   if (!BLOCKS) {
-    word = (t * 32 + lane) < nelem_words ? __ldg(bitmap + t * 32 + lane) : 0u;
+    const int64_t wi = t * 32 + lane;
+    if (wi < nelem_words) {
+      if (pm.n == 0) {
+        word = __ldg(bitmap + wi);
+      } else {
+        // union of the W ranks' bitmaps read straight from peer memory (NVLink) — the
+        // exchange kernel then only has to move the sketch table (BlockMask.union, sparse.py:55-58)
+#pragma unroll
+        for (int q = 0; q < kMaxWorld; ++q)
+          if (q < pm.n) word |= __ldcg(pm.p[q] + wi);
+      }
+    }
   } else {
     word = expand_blocks(bitmap, e0, dim, bs);
   }
@@ -651,7 +662,8 @@ __global__ void __launch_bounds__(kThreads)
 k_decode(const uint32_t* __restrict__ bitmap, int64_t dim, int64_t bs,
          const float* __restrict__ table, float workers, float inv_workers, int workers_pow2,
          float* __restrict__ out, float4* __restrict__ zt, int64_t zt_n4,
-         unsigned long long* __restrict__ zc, const __grid_constant__ HashParams hp) {
+         unsigned long long* __restrict__ zc, const __grid_constant__ HashParams hp,
+         const __grid_constant__ PeerMaps pm) {
   if (zt != nullptr) {
     const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < zt_n4; i += (int64_t)gridDim.x * kThreads)
@@ -671,11 +683,11 @@ k_decode(const uint32_t* __restrict__ bitmap, int64_t dim, int64_t bs,
   const int64_t nw = (int64_t)gridDim.x * kWarps;
 
   int64_t t = (int64_t)blockIdx.x * kWarps + wib;
-  uint32_t wnext = t < ntiles ? decode_word<BLOCKS>(bitmap, t, lane, dim, bs, nelem_words) : 0u;
+  uint32_t wnext = t < ntiles ? decode_word<BLOCKS>(bitmap, pm, t, lane, dim, bs, nelem_words) : 0u;
   for (; t < ntiles; t += nw) {
     const int64_t base = t * kTile;
     const uint32_t word = wnext;  // prefetched one tile ahead
-    if (t + nw < ntiles) wnext = decode_word<BLOCKS>(bitmap, t + nw, lane, dim, bs, nelem_words);
+    if (t + nw < ntiles) wnext = decode_word<BLOCKS>(bitmap, pm, t + nw, lane, dim, bs, nelem_words);
     // warp exclusive scan of the per-lane set counts -> queue of set positions
     const int cnt = __popc(word);
     int pre = cnt;
@@ -1027,7 +1039,7 @@ cudaError_t launch_compress(const Plan& p, const float* g, uint32_t* bitmap, flo
 
 template <int R>
 static void launch_decode_r(const Plan& p, const uint32_t* bitmap, const float* table, int workers,
-                            float* out, float* zt, unsigned long long* zc, cudaStream_t st) {
+                            float* out, float* zt, unsigned long long* zc, const PeerMaps& pm, cudaStream_t st) {
   const int64_t ntiles = (p.dim + kTile - 1) / kTile;
   const int grid = grid_for(ntiles, 4);
   const int pow2 = (workers & (workers - 1)) == 0;
@@ -1036,17 +1048,20 @@ static void launch_decode_r(const Plan& p, const uint32_t* bitmap, const float* 
   float4* z4 = reinterpret_cast<float4*>(zt);
   if (p.block_size == 1)
     launch_ex(k_decode<R, false>, grid, kThreads, 0, st, bitmap, p.dim, (int64_t)1, table, (float)workers, inv, pow2,
-              out, z4, zn4, zc, p.hp);
+              out, z4, zn4, zc, p.hp, pm);
   else
     launch_ex(k_decode<R, true>, grid, kThreads, 0, st, bitmap, p.dim, p.block_size, table, (float)workers, inv,
-              pow2, out, z4, zn4, zc, p.hp);
+              pow2, out, z4, zn4, zc, p.hp, pm);
 }
 
 cudaError_t launch_decode(const Plan& p, const uint32_t* bitmap, const float* table, int workers,
-                          float* out, cudaStream_t st, float* zero_table, unsigned long long* zero_counters) {
+                          float* out, cudaStream_t st, float* zero_table, unsigned long long* zero_counters,
+                          const PeerMaps* peers) {
+  PeerMaps pm{};
+  if (peers != nullptr && p.block_size == 1) pm = *peers;
   switch (p.hp.rows) {
 #define S2_CASE(r) \
-  case r: launch_decode_r<r>(p, bitmap, table, workers, out, zero_table, zero_counters, st); break;
+  case r: launch_decode_r<r>(p, bitmap, table, workers, out, zero_table, zero_counters, pm, st); break;
     S2_CASE(1) S2_CASE(2) S2_CASE(3) S2_CASE(4) S2_CASE(5) S2_CASE(6) S2_CASE(7) S2_CASE(8)
     S2_CASE(9) S2_CASE(10) S2_CASE(11) S2_CASE(12) S2_CASE(13) S2_CASE(14) S2_CASE(15) S2_CASE(16)
 #undef S2_CASE

@@ -21,9 +21,15 @@ struct Plan {
 
 cudaError_t launch_compress(const Plan& p, const float* g, uint32_t* bitmap, float* table,
                             unsigned long long* counters, int mode, cudaStream_t st, bool prezeroed = false);
+constexpr int kMaxWorld = 8;
+// bitmaps of every rank (peer-mapped) whose OR the decode reads directly; n = 0: use `bitmap`
+struct PeerMaps {
+  const uint32_t* p[kMaxWorld];
+  int n;
+};
 cudaError_t launch_decode(const Plan& p, const uint32_t* bitmap, const float* table, int workers,
                           float* out, cudaStream_t st, float* zero_table = nullptr,
-                          unsigned long long* zero_counters = nullptr);
+                          unsigned long long* zero_counters = nullptr, const PeerMaps* peers = nullptr);
 cudaError_t launch_bitmap_or(int64_t words, const uint32_t* stacked, int nmasks, uint32_t* out,
                              cudaStream_t st);
 cudaError_t launch_table_sum(int64_t cells, const float* stacked, int ntables, float* out,
@@ -39,7 +45,6 @@ cudaError_t launch_pairs(const Plan& p, const int64_t* idx, const float* vals, i
                          float* out, cudaStream_t st);
 
 // NVLink peer-memory exchange (s2_p2p.cu)
-constexpr int kMaxWorld = 8;
 struct P2PArgs {
   char* base[kMaxWorld];  // arena base of every rank (self included), mapped in this process
   int64_t off_table[2], off_bitmap[2], off_union[2];
@@ -49,6 +54,7 @@ struct P2PArgs {
   int64_t words;  // bitmap words, padded to a multiple of 4 * world
   int world, rank, cur;
   int oneshot;                // 1: one-shot exchange (single barrier), 0: two-shot
+  int table_only;             // 1: bitmaps are OR-ed by the decode from peer memory (no bitmap exchange)
   unsigned long long* trace;  // optional: per-CTA globaltimer stamps [G][8] (S2_P2P_TRACE=1)
 };
 cudaError_t launch_p2p_aggregate(const P2PArgs& a, int grid, cudaStream_t st);

@@ -167,6 +167,7 @@ __device__ __forceinline__ void gather_batch(const P2PArgs& a, int64_t i0, int64
 template <int W>
 __global__ void __launch_bounds__(kP2PThreads) k_p2p_aggregate(const __grid_constant__ P2PArgs a) {
   __shared__ uint32_t s_ep;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic launch: compress must be complete
   S2_TRACE(0);
   if (threadIdx.x == 0) {
     uint32_t* e = reinterpret_cast<uint32_t*>(a.base[a.rank] + a.off_epoch) + blockIdx.x;
@@ -176,7 +177,7 @@ __global__ void __launch_bounds__(kP2PThreads) k_p2p_aggregate(const __grid_cons
   __syncthreads();
   const uint32_t ep = s_ep;
   const int64_t t4 = a.cells / 4 / W;  // 16-byte vectors per slice: table ...
-  const int64_t w4 = a.words / 4 / W;  // ... and bitmap
+  const int64_t w4 = a.table_only ? 0 : a.words / 4 / W;  // ... and bitmap (unless the decode ORs them)
   int64_t lo, hi;
   chunk_of(t4 + w4, lo, hi);
   cross_rank_barrier<W>(a, a.off_flags_a, ep);
@@ -198,6 +199,7 @@ __global__ void __launch_bounds__(kP2PThreads) k_p2p_aggregate(const __grid_cons
 template <int W>
 __global__ void __launch_bounds__(kP2PThreads) k_p2p_oneshot(const __grid_constant__ P2PArgs a) {
   __shared__ uint32_t s_ep;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic launch: compress must be complete
   S2_TRACE(0);
   if (threadIdx.x == 0) {
     uint32_t* e = reinterpret_cast<uint32_t*>(a.base[a.rank] + a.off_epoch) + blockIdx.x;
@@ -206,7 +208,7 @@ __global__ void __launch_bounds__(kP2PThreads) k_p2p_oneshot(const __grid_consta
   }
   __syncthreads();
   const int me = a.rank, cur = a.cur;
-  const int64_t t4 = a.cells / 4, w4 = a.words / 4;
+  const int64_t t4 = a.cells / 4, w4 = a.table_only ? 0 : a.words / 4;
   int64_t lo, hi;
   chunk_of(t4 + w4, lo, hi);
   cross_rank_barrier<W>(a, a.off_flags_a, s_ep);
@@ -253,31 +255,45 @@ __global__ void __launch_bounds__(kP2PThreads) k_p2p_oneshot(const __grid_consta
   S2_TRACE(4);
 }
 
+static cudaError_t launch_coop(const void* fn, const P2PArgs& a, int grid, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kP2PThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;  // all G CTAs co-resident (they wait on peers)
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  void* args[] = {const_cast<P2PArgs*>(&a)};
+  return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
 cudaError_t launch_p2p_aggregate(const P2PArgs& a, int grid, cudaStream_t st) {
+  const void* fn = nullptr;
   if (a.oneshot) {
-    void* args[] = {const_cast<P2PArgs*>(&a)};
-    const void* fn = nullptr;
     switch (a.world) {
       case 2: fn = (const void*)k_p2p_oneshot<2>; break;
       case 3: fn = (const void*)k_p2p_oneshot<3>; break;
       case 4: fn = (const void*)k_p2p_oneshot<4>; break;
       default: return cudaErrorInvalidValue;
     }
-    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kP2PThreads), args, 0, st);
+  } else {
+    switch (a.world) {
+      case 2: fn = (const void*)k_p2p_aggregate<2>; break;
+      case 3: fn = (const void*)k_p2p_aggregate<3>; break;
+      case 4: fn = (const void*)k_p2p_aggregate<4>; break;
+      case 5: fn = (const void*)k_p2p_aggregate<5>; break;
+      case 6: fn = (const void*)k_p2p_aggregate<6>; break;
+      case 7: fn = (const void*)k_p2p_aggregate<7>; break;
+      case 8: fn = (const void*)k_p2p_aggregate<8>; break;
+      default: return cudaErrorInvalidValue;
+    }
   }
-  void* args[] = {const_cast<P2PArgs*>(&a)};
-  const void* fn = nullptr;
-  switch (a.world) {
-    case 2: fn = (const void*)k_p2p_aggregate<2>; break;
-    case 3: fn = (const void*)k_p2p_aggregate<3>; break;
-    case 4: fn = (const void*)k_p2p_aggregate<4>; break;
-    case 5: fn = (const void*)k_p2p_aggregate<5>; break;
-    case 6: fn = (const void*)k_p2p_aggregate<6>; break;
-    case 7: fn = (const void*)k_p2p_aggregate<7>; break;
-    case 8: fn = (const void*)k_p2p_aggregate<8>; break;
-    default: return cudaErrorInvalidValue;
-  }
-  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kP2PThreads), args, 0, st);
+  return launch_coop(fn, a, grid, st);
 }
 
 }  // namespace s2
