@@ -335,7 +335,7 @@ static int setup_p2p(s2_plan* plan) {
   // W <= 4: the decode ORs the W bitmaps straight from peer memory, the exchange moves only the
   // table; above that the OR is reduce-scattered with the table (less NVLink traffic per rank)
   const char* bd_env = getenv("S2_P2P_BITMAP_IN_DECODE_MAXW");
-  const int bd_maxw = bd_env ? atoi(bd_env) : 4;
+  const int bd_maxw = bd_env ? atoi(bd_env) : 0;  // off by default: remote word latency stalls the decode
   a.table_only = (W <= bd_maxw && plan->p.block_size == 1) ? 1 : 0;
   for (int k = 0; k < 2; ++k) a.off_tsum[k] = a.oneshot ? take(cells * 4) : a.off_table[k];
   a.cells = cells;
