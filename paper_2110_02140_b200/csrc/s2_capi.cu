@@ -11,6 +11,7 @@
 #include "s2.h"
 #include "s2_common.cuh"
 #include "s2_kernels.h"
+#include "s2_decode.cuh"
 
 using s2::HashParams;
 using s2::Plan;
@@ -37,6 +38,8 @@ struct s2_plan {
   char* peer[s2::kMaxWorld] = {};
   s2::P2PArgs pa{};
   int p2p_grid = 0;
+  bool fused = false;  // W > 1: one k_xdecode launch replaces exchange + decode
+  int x_grid = 0;
 };
 
 namespace {
@@ -327,8 +330,9 @@ static int setup_p2p(s2_plan* plan) {
   for (int k = 0; k < 2; ++k) a.off_union[k] = take(words * 4);
   a.off_flags_a = take((int64_t)W * G * 4);
   a.off_flags_b = take((int64_t)W * G * 4);
-  a.off_epoch = take((int64_t)G * 4);
+  a.off_epoch = take((int64_t)8 * G * 4);  // per-CTA epochs (fused grid <= 8 CTAs/SM)
   a.off_error = take(256);
+  a.off_lsync = take(256);
   const char* os_env = getenv("S2_P2P_ONESHOT_MAXW");
   const int oneshot_maxw = os_env ? atoi(os_env) : 2;
   a.oneshot = (W <= oneshot_maxw && W <= 4) ? 1 : 0;
@@ -383,11 +387,22 @@ static int setup_p2p(s2_plan* plan) {
   }
   plan->p2p_grid = G;
   plan->p2p = true;
+  // fused exchange+decode (k_xdecode): cooperative grid = co-resident CTAs (<= 4 per SM)
+  plan->fused = false;
+  const char* fz = getenv("S2_FUSED");
+  if (!(fz && atoi(fz) == 0) && plan->p.block_size == 1) {
+    s2::DecodeCtx probe{};
+    probe.dim = plan->p.dim;
+    probe.bs = 1;
+    cudaError_t e = s2::xdecode_grid(plan->p.hp, W, a.oneshot, &plan->x_grid);
+    if (e == cudaSuccess && plan->x_grid > 0) plan->fused = true;
+    else cudaGetLastError();
+  }
   a.trace = nullptr;
   const char* tr = getenv("S2_P2P_TRACE");
   if (tr && atoi(tr)) {
-    S2_CUDA(cudaMalloc(&a.trace, sizeof(unsigned long long) * 8 * G), "cudaMalloc(trace)");
-    S2_CUDA(cudaMemset(a.trace, 0, sizeof(unsigned long long) * 8 * G), "cudaMemset(trace)");
+    S2_CUDA(cudaMalloc(&a.trace, sizeof(unsigned long long) * 64 * G), "cudaMalloc(trace)");
+    S2_CUDA(cudaMemset(a.trace, 0, sizeof(unsigned long long) * 64 * G), "cudaMemset(trace)");
   }
   // the ping-pong tables of s2_reduce live in the arena; counters stay private
   for (int k = 0; k < 2; ++k) {
@@ -493,6 +508,24 @@ int s2_reduce(s2_plan* plan, const float* g, float* out, uint64_t* counters, voi
           "s2_reduce/compress");
   if (plan->ev[1]) cudaEventRecord(plan->ev[1], st);
   const uint32_t* un = bitmap;
+  if (plan->world > 1 && plan->p2p && plan->fused) {
+    plan->pa.cur = cur;
+    s2::DecodeCtx dc{};
+    dc.out = out;
+    dc.dim = plan->p.dim;
+    dc.bs = 1;
+    dc.workers = (float)plan->world;
+    dc.inv_workers = 1.0f / (float)plan->world;
+    dc.workers_pow2 = (plan->world & (plan->world - 1)) == 0;
+    if (plan->ev[1]) cudaEventRecord(plan->ev[1], st);
+    if (plan->ev[2]) cudaEventRecord(plan->ev[2], st);
+    S2_CUDA(s2::launch_xdecode(plan->pa, dc, plan->p.hp, plan->x_grid, plan->tables[nxt],
+                               ((int64_t)plan->p.hp.rows * plan->p.hp.cols + 3) / 4, plan->counters[nxt], st),
+            "s2_reduce/fused exchange+decode");
+    if (plan->ev[3]) cudaEventRecord(plan->ev[3], st);
+    plan->phase = nxt;
+    return S2_OK;
+  }
   if (plan->world > 1) {
     if (plan->p2p) {
       plan->pa.cur = cur;
@@ -529,7 +562,7 @@ int s2_p2p_error(const s2_plan* plan) {
 
 int s2_p2p_trace(const s2_plan* plan, uint64_t* host, int64_t n) {
   if (!plan || !plan->p2p || !plan->pa.trace) return fail(S2_EINVAL, "no p2p trace (set S2_P2P_TRACE=1)");
-  const int64_t m = (int64_t)plan->p2p_grid * 8 < n ? (int64_t)plan->p2p_grid * 8 : n;
+  const int64_t m = (int64_t)plan->p2p_grid * 64 < n ? (int64_t)plan->p2p_grid * 64 : n;
   S2_CUDA(cudaMemcpy(host, plan->pa.trace, sizeof(uint64_t) * m, cudaMemcpyDeviceToHost), "trace copy");
   return S2_OK;
 }

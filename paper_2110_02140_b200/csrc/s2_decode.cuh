@@ -1,0 +1,162 @@
+// s2_decode.cuh — the K4 decode body (sparse_decompress, sparse.py:199-214 + CountSketchTable.query,
+// sketch.py:114-128), shared by the standalone decode kernel (s2_kernels.cu) and the fused
+// exchange+decode kernel (s2_p2p.cu).
+#pragma once
+
+#include "s2_common.cuh"
+#include "s2_kernels.h"
+
+namespace s2 {
+
+constexpr int kDecTile = 1024;  // elements per warp tile (32 bitmap words)
+
+// lower median (element (R-1)/2 of the sorted estimates, sketch.py:127-128)
+template <int R>
+__device__ __forceinline__ float lower_median(float (&e)[R]) {
+  if constexpr (R == 1) {
+    return e[0];
+  } else if constexpr (R == 2) {
+    return fminf(e[0], e[1]);
+  } else if constexpr (R == 3) {
+    return fmaxf(fminf(e[0], e[1]), fminf(fmaxf(e[0], e[1]), e[2]));
+  } else {
+    // odd-even transposition sort network, fully unrolled in registers
+#pragma unroll
+    for (int p = 0; p < R; ++p) {
+#pragma unroll
+      for (int a = (p & 1); a + 1 < R; a += 2) {
+        const float lo = fminf(e[a], e[a + 1]);
+        const float hi = fmaxf(e[a], e[a + 1]);
+        e[a] = lo;
+        e[a + 1] = hi;
+      }
+    }
+    return e[(R - 1) / 2];
+  }
+}
+
+template <int R>
+__device__ __forceinline__ float query_one(uint64_t i, const float* __restrict__ table,
+                                           const HashParams& hp) {
+  const size_t cols = hp.cols;
+  float e[R];
+  if (hp.mode == kInjective) {
+#pragma unroll
+    for (int j = 0; j < R; ++j) e[j] = __ldg(table + j * cols + i);
+  } else {
+    const uint64_t x = index_term(i);
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const uint64_t w = mix64(hp.seed[j] + x);
+      const float t = __ldg(table + j * cols + bucket_of(w, hp));
+      e[j] = (w >> 63) ? -t : t;
+    }
+  }
+  return lower_median<R>(e);
+}
+
+template <bool BLOCKS>
+__device__ __forceinline__ uint32_t decode_word(const uint32_t* __restrict__ bitmap, const PeerMaps& pm, int64_t t,
+                                               int lane, int64_t dim, int64_t bs, int64_t nelem_words) {
+  const int64_t e0 = t * kDecTile + 32 * lane;
+  uint32_t word = 0;
+  if (!BLOCKS) {
+    const int64_t wi = t * 32 + lane;
+    if (wi < nelem_words) {
+      if (pm.n == 0) {
+        word = __ldg(bitmap + wi);
+      } else {
+        // union of the W ranks' bitmaps read straight from peer memory (NVLink) — the
+        // exchange kernel then only has to move the sketch table (BlockMask.union, sparse.py:55-58)
+#pragma unroll
+        for (int q = 0; q < kMaxWorld; ++q)
+          if (q < pm.n) word |= __ldcg(pm.p[q] + wi);
+      }
+    }
+  } else {
+    word = expand_blocks(bitmap, e0, dim, bs);
+  }
+  if (e0 + 32 > dim) word &= e0 >= dim ? 0u : range_mask(0, (int)(dim - e0));
+  return word;
+}
+
+struct DecodeCtx {
+  const uint32_t* bitmap;  // union bitmap (ignored when PeerMaps n > 0)
+  const float* table;      // summed sketch table
+  float* out;
+  int64_t dim, bs;
+  float workers, inv_workers;
+  int workers_pow2;
+};
+
+__device__ __forceinline__ void zero_next(float4* __restrict__ zt, int64_t zt_n4, unsigned long long* __restrict__ zc) {
+  if (zt != nullptr) {
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < zt_n4; i += (int64_t)gridDim.x * blockDim.x)
+      zt[i] = z;
+  }
+  if (zc != nullptr && blockIdx.x == 0 && threadIdx.x < S2_NUM_COUNTERS) zc[threadIdx.x] = 0ull;
+}
+
+// Decode warp tiles t0, t0+tstep, ... < tend (one warp).  Per tile: the bitmap word is
+// prefetched one tile ahead, set positions are compacted by a warp scan into q, values
+// (r gathers + lower median + IEEE /W) land in vals, and the tile is written as dense
+// float4 streaming stores (zeros included).
+template <int R, bool BLOCKS>
+__device__ __forceinline__ void decode_range(const DecodeCtx& c, const PeerMaps& pm, int64_t t0, int64_t tstep,
+                                             int64_t tend, const HashParams& hp, uint16_t* q, float* vals) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nelem_words = (c.dim + 31) / 32;
+  const int64_t dim = c.dim;
+  int64_t t = t0;
+  uint32_t wnext = t < tend ? decode_word<BLOCKS>(c.bitmap, pm, t, lane, dim, c.bs, nelem_words) : 0u;
+  for (; t < tend; t += tstep) {
+    const int64_t base = t * kDecTile;
+    const uint32_t word = wnext;
+    if (t + tstep < tend) wnext = decode_word<BLOCKS>(c.bitmap, pm, t + tstep, lane, dim, c.bs, nelem_words);
+    const int cnt = __popc(word);
+    int pre = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(kFull, pre, o);
+      if (lane >= o) pre += n;
+    }
+    const int total = __shfl_sync(kFull, pre, 31);
+    pre -= cnt;
+    for (uint32_t w = word; w; w &= w - 1u) q[pre++] = (uint16_t)(lane * 32 + (__ffs(w) - 1));
+    __syncwarp();
+    for (int s = lane; s < total; s += 32) {
+      const int pos = q[s];
+      // IEEE division: sparse.py:213 divides the float64 query by workers; x*2^-k is exact
+      const float qv = query_one<R>((uint64_t)(base + pos), c.table, hp);
+      vals[pos] = c.workers_pow2 ? qv * c.inv_workers : __fdiv_rn(qv, c.workers);
+    }
+    __syncwarp();
+    const bool full = base + kDecTile <= dim;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t wk = __shfl_sync(kFull, word, 4 * k + (lane >> 3));
+      const uint32_t nib = (wk >> ((lane & 7) * 4)) & 0xFu;
+      float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (nib) {
+        const float4 sv = *reinterpret_cast<const float4*>(vals + k * 128 + lane * 4);
+        o.x = (nib & 1u) ? sv.x : 0.f;
+        o.y = (nib & 2u) ? sv.y : 0.f;
+        o.z = (nib & 4u) ? sv.z : 0.f;
+        o.w = (nib & 8u) ? sv.w : 0.f;
+      }
+      const int64_t e = base + k * 128 + lane * 4;
+      if (full) {
+        __stcs(reinterpret_cast<float4*>(c.out + e), o);
+      } else {
+        if (e + 0 < dim) c.out[e + 0] = o.x;
+        if (e + 1 < dim) c.out[e + 1] = o.y;
+        if (e + 2 < dim) c.out[e + 2] = o.z;
+        if (e + 3 < dim) c.out[e + 3] = o.w;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace s2

@@ -50,6 +50,7 @@ struct P2PArgs {
   int64_t off_table[2], off_bitmap[2], off_union[2];
   int64_t off_flags_a, off_flags_b, off_epoch, off_error;
   int64_t off_tsum[2];  // one-shot: private summed tables
+  int64_t off_lsync;    // fused kernel: local arrival counter (u64) + release word (u32)
   int64_t cells;  // table cells, padded to a multiple of 4 * world
   int64_t words;  // bitmap words, padded to a multiple of 4 * world
   int world, rank, cur;
@@ -58,5 +59,10 @@ struct P2PArgs {
   unsigned long long* trace;  // optional: per-CTA globaltimer stamps [G][8] (S2_P2P_TRACE=1)
 };
 cudaError_t launch_p2p_aggregate(const P2PArgs& a, int grid, cudaStream_t st);
+struct DecodeCtx;
+cudaError_t xdecode_grid(const HashParams& hp, int world, int oneshot, int* grid);
+// fused exchange + decode (W > 1); cudaErrorNotSupported for (rows, world) without an instantiation
+cudaError_t launch_xdecode(const P2PArgs& a, const DecodeCtx& dc, const HashParams& hp, int grid, float* zt,
+                           int64_t zt_n4, unsigned long long* zc, cudaStream_t st);
 
 }  // namespace s2

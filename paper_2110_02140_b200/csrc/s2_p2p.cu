@@ -20,6 +20,7 @@
 // CTAs are co-resident.  Epochs live in the arena (one counter per CTA), which keeps
 // the kernel replayable inside a CUDA graph.
 #include "s2_kernels.h"
+#include "s2_decode.cuh"
 
 namespace s2 {
 
@@ -253,6 +254,261 @@ __global__ void __launch_bounds__(kP2PThreads) k_p2p_oneshot(const __grid_consta
   }
   __syncthreads();
   S2_TRACE(4);
+}
+
+// ============================================================ fused exchange + decode
+//
+// k_xdecode replaces k_p2p_* + k_decode for W > 1: one cooperative launch per reduce
+// after the compress.  Cross-rank synchronisation is hierarchical — CTA 0 exchanges one
+// flag per rank pair over NVLink and releases the local CTAs through a gpu-scope word —
+// and the local grid barrier before the decode is a 64-bit arrival counter.  CTA b
+// computes the union bitmap words of ITS OWN decode tile range (OR of the W ranks'
+// bitmaps, peer loads batched with the table loads), so only the table needs the grid
+// barrier.  Table: one-shot (W <= 2 by default) or two-shot (reduce-scatter, barrier,
+// all-gather).
+struct XSync {
+  unsigned long long* arrive;  // local arrival counter (cumulative)
+  uint32_t* release;           // CTA 0 -> local CTAs: last cross-rank epoch passed (x2 per call)
+};
+
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_gpu64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// all CTAs of this grid arrive; returns when `target` arrivals were counted
+__device__ __forceinline__ void local_arrive_wait(unsigned long long* arrive, unsigned long long target,
+                                                  bool wait_all) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(arrive, 1ull);
+    if (wait_all)
+      while (ld_acquire_gpu64(arrive) < target) {
+      }
+  }
+  __syncthreads();
+}
+
+// CTA 0 <-> CTA 0 of every rank (flag slot [rank] of each rank's array), then release locally
+template <int W>
+__device__ __forceinline__ void rank_barrier(const P2PArgs& a, int64_t off_flags, uint32_t ep, uint32_t* release,
+                                             uint32_t rel_val) {
+  if (blockIdx.x == 0) {
+    if (threadIdx.x < W) {
+      const int q = threadIdx.x;
+      st_release_sys(reinterpret_cast<uint32_t*>(a.base[q] + off_flags) + a.rank, ep);
+      const uint32_t* mine = reinterpret_cast<const uint32_t*>(a.base[a.rank] + off_flags) + q;
+      uint64_t t0 = 0;
+      for (int spin = 0; (int32_t)(ld_acquire_sys(mine) - ep) < 0; ++spin) {
+        if ((spin & 1023) == 1023) {
+          const uint64_t now = globaltimer();
+          if (t0 == 0) t0 = now;
+          else if (now - t0 > 10000000000ull) {
+            atomicOr(reinterpret_cast<uint32_t*>(a.base[a.rank] + a.off_error), 1u);
+            break;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) st_release_gpu(release, rel_val);
+  } else if (threadIdx.x == 0) {
+    uint64_t t0 = 0;
+    for (int spin = 0; (int32_t)(ld_acquire_gpu(release) - rel_val) < 0; ++spin) {
+      if ((spin & 1023) == 1023) {
+        const uint64_t now = globaltimer();
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > 10000000000ull) break;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+template <int R, int W, bool ONESHOT>
+__global__ void __launch_bounds__(256, 4)
+k_xdecode(const __grid_constant__ P2PArgs a, const __grid_constant__ DecodeCtx dc, const __grid_constant__ HashParams hp,
+          float4* __restrict__ zt, int64_t zt_n4, unsigned long long* __restrict__ zc) {
+  extern __shared__ __align__(16) unsigned char x_smem[];  // vals [8][1024] f32 | queue [8][1024] u16
+  float (*s_v)[kDecTile] = reinterpret_cast<float (*)[kDecTile]>(x_smem);
+  uint16_t (*s_q)[kDecTile] = reinterpret_cast<uint16_t (*)[kDecTile]>(x_smem + 8 * kDecTile * 4);
+  __shared__ uint32_t s_ep;
+  __shared__ int s_next;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  S2_TRACE(0);
+  const int me = a.rank, cur = a.cur, G = gridDim.x;
+  if (threadIdx.x == 0) {
+    uint32_t* e = reinterpret_cast<uint32_t*>(a.base[me] + a.off_epoch) + blockIdx.x;
+    s_ep = *e + 1u;
+    *e = s_ep;
+    s_next = 0;
+  }
+  __syncthreads();
+  const uint32_t ep = s_ep;
+  unsigned long long* arrive = reinterpret_cast<unsigned long long*>(a.base[me] + a.off_lsync);
+  uint32_t* release = reinterpret_cast<uint32_t*>(a.base[me] + a.off_lsync + 8);
+  constexpr int K = ONESHOT ? 1 : 2;  // local arrivals per call
+
+  // barrier 1: every rank's compress is complete
+  rank_barrier<W>(a, a.off_flags_a, ep, release, 2u * ep - 1u);
+  S2_TRACE(1);
+  // the NEXT ping-pong table held the previous reduce, which peers read before reaching
+  // barrier 1 of this one — only now may it be zeroed for the next compress
+  zero_next(zt, zt_n4, zc);
+
+  // this CTA's decode tiles and their union words
+  const int64_t ntiles = (dc.dim + kDecTile - 1) / kDecTile;
+  const int64_t per = (ntiles + G - 1) / G;
+  const int64_t tb = (int64_t)blockIdx.x * per < ntiles ? (int64_t)blockIdx.x * per : ntiles;
+  const int64_t te = tb + per < ntiles ? tb + per : ntiles;
+  const int64_t nwords = (dc.dim + 31) / 32;
+  uint32_t* un = reinterpret_cast<uint32_t*>(a.base[me] + a.off_union[cur]);
+  {
+    const int64_t w0 = tb * 32, w1 = te * 32 < nwords ? te * 32 : nwords;
+    for (int64_t i = w0 + threadIdx.x; i < w1; i += blockDim.x) {
+      uint32_t v[W];
+#pragma unroll
+      for (int q = 0; q < W; ++q) v[q] = __ldcg(reinterpret_cast<const uint32_t*>(a.base[q] + a.off_bitmap[cur]) + i);
+      uint32_t o = v[0];
+#pragma unroll
+      for (int q = 1; q < W; ++q) o |= v[q];
+      un[i] = o;
+    }
+  }
+  // table
+  if (ONESHOT) {
+    const int64_t t4 = a.cells / 4;
+    int64_t lo, hi;
+    chunk_of(t4, lo, hi);
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+      uint4 v[W];
+#pragma unroll
+      for (int q = 0; q < W; ++q) v[q] = __ldcg(reinterpret_cast<const uint4*>(a.base[q] + a.off_table[cur]) + i);
+      float fx = __uint_as_float(v[0].x), fy = __uint_as_float(v[0].y);
+      float fz = __uint_as_float(v[0].z), fw = __uint_as_float(v[0].w);
+#pragma unroll
+      for (int q = 1; q < W; ++q) {
+        fx += __uint_as_float(v[q].x); fy += __uint_as_float(v[q].y);
+        fz += __uint_as_float(v[q].z); fw += __uint_as_float(v[q].w);
+      }
+      reinterpret_cast<float4*>(a.base[me] + a.off_tsum[cur])[i] = make_float4(fx, fy, fz, fw);
+    }
+  } else {
+    const int64_t t4 = a.cells / 4 / W;  // per slice
+    int64_t lo, hi;
+    chunk_of(t4, lo, hi);
+    float4* dst = reinterpret_cast<float4*>(a.base[me] + a.off_table[cur]) + me * t4;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+      uint4 v[W];
+#pragma unroll
+      for (int q = 0; q < W; ++q)
+        v[q] = __ldcg(reinterpret_cast<const uint4*>(a.base[q] + a.off_table[cur]) + me * t4 + i);
+      float fx = __uint_as_float(v[0].x), fy = __uint_as_float(v[0].y);
+      float fz = __uint_as_float(v[0].z), fw = __uint_as_float(v[0].w);
+#pragma unroll
+      for (int q = 1; q < W; ++q) {
+        fx += __uint_as_float(v[q].x); fy += __uint_as_float(v[q].y);
+        fz += __uint_as_float(v[q].z); fw += __uint_as_float(v[q].w);
+      }
+      dst[i] = make_float4(fx, fy, fz, fw);
+    }
+    // barrier 2: every rank's reduced slice is final
+    local_arrive_wait(arrive, ((unsigned long long)(ep - 1) * K + 1) * G, blockIdx.x == 0);
+    rank_barrier<W>(a, a.off_flags_b, ep, release, 2u * ep);
+    float4* tab = reinterpret_cast<float4*>(a.base[me] + a.off_table[cur]);
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+      uint4 v[W];
+#pragma unroll
+      for (int q = 0; q < W; ++q)
+        if (q != me) v[q] = __ldcg(reinterpret_cast<const uint4*>(a.base[q] + a.off_table[cur]) + q * t4 + i);
+#pragma unroll
+      for (int q = 0; q < W; ++q)
+        if (q != me) tab[q * t4 + i] = *reinterpret_cast<float4*>(&v[q]);
+    }
+  }
+  S2_TRACE(2);
+  // local grid barrier: the whole summed table is in place
+  local_arrive_wait(arrive, ((unsigned long long)(ep - 1) * K + K) * G, true);
+  S2_TRACE(3);
+  // decode this CTA's tile range; warps take tiles dynamically (shared counter)
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  PeerMaps none{};
+  DecodeCtx c = dc;
+  c.bitmap = un;
+  c.table = ONESHOT ? reinterpret_cast<const float*>(a.base[me] + a.off_tsum[cur])
+                    : reinterpret_cast<const float*>(a.base[me] + a.off_table[cur]);
+  for (;;) {
+    int k = 0;
+    if (lane == 0) k = atomicAdd(&s_next, 1);
+    k = __shfl_sync(kFull, k, 0);
+    const int64_t t = tb + k;
+    if (t >= te) break;
+    decode_range<R, false>(c, none, t, 1, t + 1, hp, s_q[wib], s_v[wib]);
+  }
+  S2_TRACE(4);
+}
+
+static const void* xdecode_fn(int rows, int world, int oneshot) {
+  const void* fn = nullptr;
+#define S2_X(R, W)                                                                    \
+  if (rows == R && world == W)                                                        \
+    fn = oneshot ? (const void*)k_xdecode<R, W, true> : (const void*)k_xdecode<R, W, false>;
+  S2_X(3, 2) S2_X(3, 3) S2_X(3, 4) S2_X(3, 5) S2_X(3, 6) S2_X(3, 7) S2_X(3, 8)
+  S2_X(5, 2) S2_X(5, 3) S2_X(5, 4) S2_X(5, 5) S2_X(5, 6) S2_X(5, 7) S2_X(5, 8)
+  S2_X(1, 2) S2_X(1, 4) S2_X(1, 8)
+#undef S2_X
+  return fn;
+}
+
+constexpr int kXSmem = 8 * kDecTile * (4 + 2);
+
+cudaError_t xdecode_grid(const HashParams& hp, int world, int oneshot, int* grid) {
+  const void* fn = xdecode_fn(hp.rows, world, oneshot);
+  *grid = 0;
+  if (fn == nullptr) return cudaErrorNotSupported;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kXSmem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0, dev = 0, sms = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, kXSmem);
+  if (e != cudaSuccess) return e;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (per_sm > 4) per_sm = 4;
+  *grid = per_sm * sms;
+  return cudaSuccess;
+}
+
+cudaError_t launch_xdecode(const P2PArgs& a, const DecodeCtx& dc, const HashParams& hp, int grid, float* zt,
+                           int64_t zt_n4, unsigned long long* zc, cudaStream_t st) {
+  const void* fn = xdecode_fn(hp.rows, a.world, a.oneshot);
+  if (fn == nullptr) return cudaErrorNotSupported;
+  constexpr int kSmem = kXSmem;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  float4* z4 = reinterpret_cast<float4*>(zt);
+  void* args[] = {const_cast<P2PArgs*>(&a), const_cast<DecodeCtx*>(&dc), const_cast<HashParams*>(&hp), &z4,
+                  &zt_n4, &zc};
+  return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
 static cudaError_t launch_coop(const void* fn, const P2PArgs& a, int grid, cudaStream_t st) {

@@ -30,14 +30,16 @@ for it in range(30):
     red.reduce(g, out=out)
     torch.cuda.synchronize()
     if it >= 10:
-        G = torch.cuda.get_device_properties(0).multi_processor_count
+        G = torch.cuda.get_device_properties(0).multi_processor_count * 8
         buf = (ctypes.c_uint64 * (8 * G))()
         check(lib.s2_p2p_trace(red.plan.handle, buf, 8 * G))
         t = np.frombuffer(buf, dtype=np.uint64).reshape(G, 8)[:, :5].astype(np.int64)
+        t = t[t[:, 0] > 0]  # CTAs of the last launch
         t0 = t[:, 0].min()
-        res.append({"start_spread": int(t[:, 0].max() - t0), "barrier1": int(np.median(t[:, 1] - t[:, 0])),
-                    "phaseA": int(np.median(t[:, 2] - t[:, 1])), "barrier2": int(np.median(t[:, 3] - t[:, 2])),
-                    "phaseB": int(np.median(t[:, 4] - t[:, 3])), "total": int(t[:, 4].max() - t0)})
+        res.append({"ctas": int(len(t)), "start_spread": int(t[:, 0].max() - t0),
+                    "s0_s1": int(np.median(t[:, 1] - t[:, 0])), "s1_s2": int(np.median(t[:, 2] - t[:, 1])),
+                    "s2_s3": int(np.median(t[:, 3] - t[:, 2])), "s3_s4": int(np.median(t[:, 4] - t[:, 3])),
+                    "total": int(t[:, 4].max() - t0)})
 agg = {k: int(np.median([r[k] for r in res])) for k in res[0]}
 all_ = [None] * world
 dist.all_gather_object(all_, agg)
