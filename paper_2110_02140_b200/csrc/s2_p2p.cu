@@ -374,15 +374,31 @@ k_xdecode(const __grid_constant__ P2PArgs a, const __grid_constant__ DecodeCtx d
   const int64_t nwords = (dc.dim + 31) / 32;
   uint32_t* un = reinterpret_cast<uint32_t*>(a.base[me] + a.off_union[cur]);
   {
-    const int64_t w0 = tb * 32, w1 = te * 32 < nwords ? te * 32 : nwords;
-    for (int64_t i = w0 + threadIdx.x; i < w1; i += blockDim.x) {
-      uint32_t v[W];
+    // union words of [tb, te) tiles: 32 words per tile -> 8 uint4 per tile, W loads each (batched)
+    const int64_t v0 = tb * 8;
+    const int64_t v1 = te * 8 < (a.words / 4) ? te * 8 : (a.words / 4);
+    constexpr int B = p2p_batch<W>();
+    for (int64_t i0 = v0 + threadIdx.x; i0 < v1; i0 += B * blockDim.x) {
+      uint4 v[B][W];
 #pragma unroll
-      for (int q = 0; q < W; ++q) v[q] = __ldcg(reinterpret_cast<const uint32_t*>(a.base[q] + a.off_bitmap[cur]) + i);
-      uint32_t o = v[0];
+      for (int k = 0; k < B; ++k) {
+        const int64_t i = i0 + k * blockDim.x;
+        if (i < v1)
 #pragma unroll
-      for (int q = 1; q < W; ++q) o |= v[q];
-      un[i] = o;
+          for (int q = 0; q < W; ++q) v[k][q] = __ldcg(reinterpret_cast<const uint4*>(a.base[q] + a.off_bitmap[cur]) + i);
+      }
+#pragma unroll
+      for (int k = 0; k < B; ++k) {
+        const int64_t i = i0 + k * blockDim.x;
+        if (i < v1) {
+          uint4 o = v[k][0];
+#pragma unroll
+          for (int q = 1; q < W; ++q) {
+            o.x |= v[k][q].x; o.y |= v[k][q].y; o.z |= v[k][q].z; o.w |= v[k][q].w;
+          }
+          reinterpret_cast<uint4*>(un)[i] = o;
+        }
+      }
     }
   }
   // table
