@@ -390,7 +390,7 @@ static int setup_p2p(s2_plan* plan) {
   // fused exchange+decode (k_xdecode): cooperative grid = co-resident CTAs (<= 4 per SM)
   plan->fused = false;
   const char* fz = getenv("S2_FUSED");
-  if (!(fz && atoi(fz) == 0) && plan->p.block_size == 1) {
+  if (fz && atoi(fz) != 0 && plan->p.block_size == 1) {  // opt-in: measured slower than separate kernels
     s2::DecodeCtx probe{};
     probe.dim = plan->p.dim;
     probe.bs = 1;
