@@ -37,7 +37,12 @@ CONFIGS = {
     "resnet50": dict(dim=25_600_000, alpha=0.01, rows=3, cols=262_144, label="ResNet-50-sized 25.6M fp32, 99% sparse"),
     "bert": dict(dim=110_000_000, alpha=0.05, rows=5, cols=1_048_576, label="BERT-base-sized 110M fp32, 95% sparse"),
     "bert_np2": dict(dim=110_000_000, alpha=0.05, rows=5, cols=1_000_000, label="BERT-base 110M, 95%, 5x1,000,000"),
+    "lstm": dict(dim=200_000_000, alpha=0.001, rows=3, cols=1_048_576, grid=(200_000, 1_000),
+                 label="LSTM-LM embedding 200M fp32 (200k x 1000), 99.9% row-sparse, element bitmap"),
+    "lstm_rows": dict(dim=200_000_000, alpha=0.001, rows=3, cols=1_048_576, grid=(200_000, 1_000),
+                      num_blocks=200_000, label="LSTM-LM embedding 200M, 99.9% row-sparse, row bitmap (b=200k)"),
     "gpt2m_90": dict(dim=355_000_000, alpha=0.10, rows=3, cols=1_048_576, label="GPT-2-medium 355M, 90% sparse"),
+    "gpt2m_99": dict(dim=355_000_000, alpha=0.01, rows=3, cols=1_048_576, label="GPT-2-medium 355M, 99% sparse"),
     "gpt2m_999": dict(dim=355_000_000, alpha=0.001, rows=3, cols=262_144, label="GPT-2-medium 355M, 99.9% sparse"),
     "oracle1m": dict(dim=1_000_000, alpha=0.01, rows=3, cols=16_384, label="1M fp32, 99% sparse (configs[0])"),
 }
@@ -131,13 +136,15 @@ def reference_arm(args, cfg):
         return
     W = args.gpus
     d, rows, cols = cfg["dim"], cfg["rows"], cfg["cols"]
-    grads = [o.synthetic_gradient(d, cfg["alpha"], r) for r in range(W)]
+    nb = cfg.get("num_blocks", d)
+    grads = [o.synthetic_gradient(d, cfg["alpha"], r) if cfg.get("grid") is None else _rows_gradient_np(cfg, r)
+             for r in range(W)]
 
     def one_step(pool):
         if pool is None:
-            ps = [o.compress(grads[0], grads[0] != 0, rows, cols, 0)]
+            ps = [o.compress(grads[0], o.nonzero_flags(grads[0], nb), rows, cols, 0)]
         else:
-            ps = pool.map(_ref_compress, [(r, rows, cols) for r in range(W)])
+            ps = pool.map(_ref_compress, [(r, rows, cols, nb) for r in range(W)])
         m = o.merge(ps)
         return o.decompress(m)
 
@@ -181,9 +188,9 @@ _REF_GRADS = None
 def _ref_compress(a):
     from oracle import s2_oracle as o
 
-    r, rows, cols = a
+    r, rows, cols, nb = a
     g = _REF_GRADS[r]
-    return o.compress(g, g != 0, rows, cols, 0)
+    return o.compress(g, o.nonzero_flags(g, nb), rows, cols, 0)
 
 
 def cpu_baseline(cfg, budget_s=10.0):
@@ -191,10 +198,12 @@ def cpu_baseline(cfg, budget_s=10.0):
     from oracle import s2_oracle as o
 
     d = cfg["dim"]
-    g = o.synthetic_gradient(d, cfg["alpha"], 0)
+    g = o.synthetic_gradient(d, cfg["alpha"], 0) if cfg.get("grid") is None else \
+        _rows_gradient_np(cfg)
+    nb = cfg.get("num_blocks", d)
     n, t0 = 0, time.perf_counter()
     while True:
-        p = o.compress(g, g != 0, cfg["rows"], cfg["cols"], 0)
+        p = o.compress(g, o.nonzero_flags(g, nb), cfg["rows"], cfg["cols"], 0)
         o.decompress(o.merge([p]))
         n += 1
         if time.perf_counter() - t0 > budget_s or n >= 50:
@@ -205,11 +214,23 @@ def cpu_baseline(cfg, budget_s=10.0):
                       f"numpy {np.__version__} single-threaded; host has {os.cpu_count()} cores"}
 
 
+def _rows_gradient_np(cfg, rank=0):
+    V, H = cfg["grid"]
+    rng = np.random.default_rng(1234 + rank)
+    r = rng.choice(V, max(1, int(round(cfg["alpha"] * V))), replace=False)
+    g = np.zeros(cfg["dim"], dtype=np.float32)
+    for row in r:
+        g[row * H:(row + 1) * H] = rng.standard_normal(H).astype(np.float32)
+    return g
+
+
 def _config_json(args, cfg):
     return {"workload": f"{args.config}: {cfg['label']}, sketch {cfg['rows']}x{cfg['cols']}, W={args.gpus}",
             "dim": cfg["dim"], "nnz_per_rank": int(round(cfg["alpha"] * cfg["dim"])), "rows": cfg["rows"],
             "cols": cfg["cols"], "world": args.gpus, "parallelism": f"dp{args.gpus}",
-            "l2": f"inputs rotate over {N_ROTATE} gradient buffers ({N_ROTATE * 4 * cfg['dim'] / 1e6:.0f} MB > 126 MB L2)"}
+            "num_blocks": cfg.get("num_blocks", cfg["dim"]),
+            "l2": f"inputs rotate over {N_ROTATE if cfg['dim'] <= 50_000_000 else 2} gradient buffers "
+                  f"({(N_ROTATE if cfg['dim'] <= 50_000_000 else 2) * 4 * cfg['dim'] / 1e6:.0f} MB > 126 MB L2)"}
 
 
 # --------------------------------------------------------------------- ours
@@ -228,14 +249,15 @@ def ours(args, cfg):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2110_02140_b200 as s2
+    from paper_2110_02140_b200 import synthetic
     from paper_2110_02140_b200._lib import check, lib, ptr
-    from oracle import s2_oracle as o  # input generation only (same bytes the oracle sees)
 
     d, rows, cols = cfg["dim"], cfg["rows"], cfg["cols"]
-    red = s2.S2Reducer(d, rows=rows, cols=cols, seed=0, world=world, rank=rank)
-    grads = [torch.from_numpy(o.synthetic_gradient(d, cfg["alpha"], rank, base_seed=1234 + 1000 * k)).cuda()
-             for k in range(N_ROTATE)]
-    outs = [torch.empty(d, dtype=torch.float32, device="cuda") for _ in range(N_ROTATE)]
+    red = s2.S2Reducer(d, rows=rows, cols=cols, seed=0, world=world, rank=rank, num_blocks=cfg.get("num_blocks"))
+    gcfg = dict(dim=d, alpha=cfg["alpha"], rows=cfg.get("grid"))
+    n_rot = N_ROTATE if d <= 50_000_000 else 2  # 2 x >= 440 MB still exceeds the 126 MB L2
+    grads = [synthetic.gradient(gcfg, rank, base_seed=1234 + 1000 * k) for k in range(n_rot)]
+    outs = [torch.empty(d, dtype=torch.float32, device="cuda") for _ in range(n_rot)]
     stream = torch.cuda.current_stream()
     sp = ctypes.c_void_p(stream.cuda_stream)
     h = red.plan.handle
@@ -244,7 +266,7 @@ def ours(args, cfg):
     null = ctypes.c_void_p(0)
 
     def step(i):
-        check(lib.s2_reduce(h, gp[i % N_ROTATE], op[i % N_ROTATE], null, sp))
+        check(lib.s2_reduce(h, gp[i % n_rot], op[i % n_rot], null, sp))
 
     def barrier():
         torch.cuda.synchronize()
@@ -301,6 +323,7 @@ def ours(args, cfg):
         phases["decode"] += ev[2].elapsed_time(ev[3])
     check(lib.s2_plan_set_timing_events(h, None, 0))
     phases = {k: max_over_ranks(v / nph) for k, v in phases.items()}
+    del outs
 
     # e2e: pinned host gradient in, pinned host result out, every step's H2D and D2H inside the
     # timed region; HostPipeline overlaps step i's reduce with step i+1's H2D and i-1's D2H
@@ -334,7 +357,7 @@ def ours(args, cfg):
         return
     hbm_peak, peak_kind = peaks()
     B = 4 * d
-    words_bytes = 4 * (-(-d // 32))
+    words_bytes = 4 * (-(-cfg.get("num_blocks", d) // 32))
     table_bytes = 4 * rows * cols
     alg = {"compress": B + words_bytes + table_bytes, "decode": words_bytes + table_bytes + B}
     dom = max(("compress", "decode"), key=lambda k: phases[k])

@@ -142,3 +142,12 @@ def test_oracle_vs_live_reference_random():
         assert np.array_equal(ours.flags, rm.mask.flags)
         assert np.array_equal(ours.table, rm.table.table)
         assert np.array_equal(o.decompress(ours), rs.sparse_decompress(rm))
+
+
+def test_bench_generator_matches_oracle_recipe():
+    """bench.py draws its inputs with paper_2110_02140_b200.synthetic (the product may not import
+    oracle/); the numpy recipe must produce the oracle's bytes."""
+    from paper_2110_02140_b200 import synthetic
+
+    for d, a, r in ((10_000, 0.01, 0), (100_003, 0.05, 3)):
+        assert np.array_equal(synthetic.numpy_gradient(d, a, r), o.synthetic_gradient(d, a, r))

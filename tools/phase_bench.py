@@ -9,7 +9,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from bench import CONFIGS  # noqa: E402
-from oracle import s2_oracle as o  # noqa: E402
+from paper_2110_02140_b200 import synthetic  # noqa: E402
 import paper_2110_02140_b200 as s2  # noqa: E402
 from paper_2110_02140_b200._lib import check, lib, ptr  # noqa: E402
 
@@ -17,7 +17,7 @@ cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "resnet50"]
 d, rows, cols = cfg["dim"], cfg["rows"], cfg["cols"]
 red = s2.S2Reducer(d, rows=rows, cols=cols)
 h = red.plan.handle
-gs = [torch.from_numpy(o.synthetic_gradient(d, cfg["alpha"], 0, base_seed=1234 + 1000 * k)).cuda() for k in range(4)]
+gs = [synthetic.gradient(dict(dim=d, alpha=cfg["alpha"], rows=cfg.get("grid")), 0, base_seed=1234 + 1000 * k) for k in range(4)]
 outs = [torch.empty(d, device="cuda") for _ in range(4)]
 tab = torch.zeros(rows * cols + 4, device="cuda")
 bm = torch.zeros(-(-d // 32) + 4, dtype=torch.int32, device="cuda")

@@ -12,7 +12,7 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 from bench import CONFIGS  # noqa: E402
-from oracle import s2_oracle as o  # noqa: E402
+from paper_2110_02140_b200 import synthetic  # noqa: E402
 import paper_2110_02140_b200 as s2  # noqa: E402
 
 ap = argparse.ArgumentParser()
@@ -22,8 +22,8 @@ ap.add_argument("--block", type=int, default=0, help="num_blocks (0 = element bi
 a = ap.parse_args()
 cfg = CONFIGS[a.config]
 d = cfg["dim"]
-red = s2.S2Reducer(d, rows=cfg["rows"], cols=cfg["cols"], seed=0, num_blocks=a.block or None)
-gs = [torch.from_numpy(o.synthetic_gradient(d, cfg["alpha"], 0, base_seed=1234 + 1000 * k)).cuda() for k in range(2)]
+red = s2.S2Reducer(d, rows=cfg["rows"], cols=cfg["cols"], seed=0, num_blocks=a.block or cfg.get("num_blocks"))
+gs = [synthetic.gradient(dict(dim=d, alpha=cfg["alpha"], rows=cfg.get("grid")), 0, base_seed=1234 + 1000 * k) for k in range(2)]
 out = torch.empty(d, device="cuda")
 for i in range(a.steps):
     red.reduce(gs[i % 2], out=out)
