@@ -234,7 +234,7 @@ k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __res
   uint64_t pol = 0;
   if (LOAD == 0) {
     if (t < ntiles) load_tile(*reinterpret_cast<float4(*)[8]>(vn), g, t, dim, lane);
-  } else {
+  } else if (LOAD == 1) {
     if (lane == 0) {
       mbar_init(&s_bar[wib], 1);
       fence_barrier_init();
@@ -251,6 +251,8 @@ k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __res
 #pragma unroll
       for (int k = 0; k < 8; ++k) v[k] = vn[k < (LOAD == 0 ? 8 : 1) ? k : 0];
       if (t + nw < ntiles) load_tile(*reinterpret_cast<float4(*)[8]>(vn), g, t + nw, dim, lane);
+    } else if (LOAD == 3) {
+      load_tile(v, g, t, dim, lane);  // no prefetch: 64 registers, 4 CTAs (32 warps) per SM
     } else {
       if (t < nfull) {
         mbar_wait(&s_bar[wib], parity);
@@ -313,7 +315,7 @@ k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __res
       nnz += (unsigned)total;
       if (qn + total <= kCap) {
         int pos = qn + incl - cnt;
-        if (LOAD == 0) {
+        if (LOAD == 0 || LOAD == 3) {
           // stage the tile (8 STS.128 per lane) so the append loop can index values dynamically:
           // ~popc(m) iterations instead of 32 per-element predicated appends
           float4* st = s_tile[wib];
@@ -833,7 +835,7 @@ static int compress_variant() {
   if (v < 0) {
     const char* e = getenv("S2_COMPRESS_LOAD");
     v = e ? atoi(e) : 0;
-    if (v < 0 || v > 2) v = 0;
+    if (v < 0 || v > 3) v = 0;
   }
   return v;
 }
@@ -874,6 +876,8 @@ static void launch_compress_r(const Plan& p, const float* g, uint32_t* bitmap, f
   const int v = compress_variant();
   if (v == 0) {
     launch_compress_rm<R, 0>(p, g, bitmap, table, counters, mode, st);
+  } else if (v == 3) {
+    launch_compress_rm<R, 3>(p, g, bitmap, table, counters, mode, st);
   } else if (v == 1) {
     launch_compress_rm<R, 1>(p, g, bitmap, table, counters, mode, st);
   } else {
