@@ -121,6 +121,19 @@ int s2_compact(const s2_plan* plan, const uint32_t* bitmap, const float* g, int6
  *      sparse_merge list fold, sparse.py:174-196) -------------------------- */
 int s2_nccl_unique_id(void* out /* 128 bytes */);
 int s2_comm_init(s2_plan* plan, int world, int rank, const void* unique_id);
+/* comm modes: IPC = plan allocates a CUDA-IPC arena (default); NCCL = NCCL collectives only;
+ * EXTERNAL = caller provides symmetric memory through s2_comm_attach (e.g. torch
+ * symmetric memory with an NVLS multicast address) */
+#define S2_COMM_IPC 0
+#define S2_COMM_NCCL 1
+#define S2_COMM_EXTERNAL 2
+int s2_comm_init_mode(s2_plan* plan, int world, int rank, const void* unique_id, int mode);
+/* bytes of the per-rank exchange arena for `world` ranks (same on every rank) */
+int64_t s2_p2p_arena_bytes(s2_plan* plan, int world);
+/* attach symmetric memory: bases[q] = rank q's arena mapped in this process, mc_base =
+ * multicast (NVLS) address of the arena or 0.  With mc_base != 0 the sketch SUM and bitmap
+ * OR are reduced inside the NVSwitch (multimem.ld_reduce + multimem.st). */
+int s2_comm_attach(s2_plan* plan, const uint64_t* bases, int world, uint64_t mc_base);
 /* one-time agreement on (dim, num_blocks, rows, cols, seed) across ranks —
  * the distributed compat_key check (sparse.py:105-109, :179-187) */
 int s2_comm_check(s2_plan* plan, void* stream);

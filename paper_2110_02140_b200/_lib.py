@@ -52,6 +52,9 @@ SIGNATURES = {
     "s2_compact": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "s2_nccl_unique_id": (c_int, [c_void_p]),
     "s2_comm_init": (c_int, [c_void_p, c_int, c_int, c_void_p]),
+    "s2_comm_init_mode": (c_int, [c_void_p, c_int, c_int, c_void_p, c_int]),
+    "s2_p2p_arena_bytes": (c_int64, [c_void_p, c_int]),
+    "s2_comm_attach": (c_int, [c_void_p, POINTER(c_uint64), c_int, c_uint64]),
     "s2_comm_check": (c_int, [c_void_p, c_void_p]),
     "s2_aggregate": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "s2_reduce": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),

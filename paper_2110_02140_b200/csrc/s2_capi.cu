@@ -40,6 +40,8 @@ struct s2_plan {
   int p2p_grid = 0;
   bool fused = false;  // W > 1: one k_xdecode launch replaces exchange + decode
   int x_grid = 0;
+  int comm_mode = 0;         // S2_COMM_IPC | S2_COMM_NCCL | S2_COMM_EXTERNAL
+  bool arena_owned = false;  // cudaMalloc'd here (IPC) vs attached symmetric memory
 };
 
 namespace {
@@ -184,10 +186,11 @@ static void free_scratch(s2_plan* p) {
 
 static void free_p2p(s2_plan* p) {
   for (int q = 0; q < s2::kMaxWorld; ++q)
-    if (p->peer[q] && p->peer[q] != p->arena) cudaIpcCloseMemHandle(p->peer[q]);
+    if (p->arena_owned && p->peer[q] && p->peer[q] != p->arena) cudaIpcCloseMemHandle(p->peer[q]);
   for (int q = 0; q < s2::kMaxWorld; ++q) p->peer[q] = nullptr;
-  if (p->arena) cudaFree(p->arena);
+  if (p->arena && p->arena_owned) cudaFree(p->arena);
   p->arena = nullptr;
+  p->arena_owned = false;
   if (p->p2p) {  // tables/counters pointed into the arena / were separately allocated
     p->tables[0] = p->tables[1] = nullptr;
   }
@@ -310,12 +313,9 @@ static int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 // One cudaMalloc arena per rank, exported with CUDA IPC and mapped by every peer:
 //   tables[2] | bitmaps[2] | unions[2] | flags_a[W*G] | flags_b[W*G] | epochs[G]
 // The handles travel through one ncclAllGather.
-static int setup_p2p(s2_plan* plan) {
-  const int W = plan->world;
-  int dev = 0, sms = 0;
-  S2_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
-  S2_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sm count");
-  const int G = sms;
+// Arena layout (identical on every rank):
+//   tables[2] | bitmaps[2] | unions[2] | flags_a[W*G] | flags_b[W*G] | epochs[8G] | error | lsync | tsum[2]?
+static int64_t layout_p2p(s2_plan* plan, int W, int G) {
   const int64_t cells = round_up((int64_t)plan->p.hp.rows * plan->p.hp.cols, 4 * W);
   const int64_t words = round_up(plan->p.words, 4 * W);
   s2::P2PArgs& a = plan->pa;
@@ -336,19 +336,69 @@ static int setup_p2p(s2_plan* plan) {
   const char* os_env = getenv("S2_P2P_ONESHOT_MAXW");
   const int oneshot_maxw = os_env ? atoi(os_env) : 2;
   a.oneshot = (W <= oneshot_maxw && W <= 4) ? 1 : 0;
-  // W <= 4: the decode ORs the W bitmaps straight from peer memory, the exchange moves only the
-  // table; above that the OR is reduce-scattered with the table (less NVLink traffic per rank)
+  // optional: the decode ORs the W bitmaps straight from peer memory and the exchange moves only
+  // the table (off by default: the per-tile NVLink latency stalls the decode)
   const char* bd_env = getenv("S2_P2P_BITMAP_IN_DECODE_MAXW");
-  const int bd_maxw = bd_env ? atoi(bd_env) : 0;  // off by default: remote word latency stalls the decode
+  const int bd_maxw = bd_env ? atoi(bd_env) : 0;
   a.table_only = (W <= bd_maxw && plan->p.block_size == 1) ? 1 : 0;
   for (int k = 0; k < 2; ++k) a.off_tsum[k] = a.oneshot ? take(cells * 4) : a.off_table[k];
   a.cells = cells;
   a.words = words;
   a.world = W;
   a.rank = plan->rank;
+  a.mc = nullptr;
+  a.nvls = 0;
+  return off;
+}
+
+static int sm_count(int* G) {
+  int dev = 0;
+  S2_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
+  S2_CUDA(cudaDeviceGetAttribute(G, cudaDevAttrMultiProcessorCount, dev), "sm count");
+  return S2_OK;
+}
+
+// base pointers known: plan tables into the arena, counters, trace, fused-kernel grid
+static int finish_p2p(s2_plan* plan, int G) {
+  s2::P2PArgs& a = plan->pa;
+  const int W = plan->world;
+  plan->p2p_grid = G;
+  plan->p2p = true;
+  a.trace = nullptr;
+  const char* tr = getenv("S2_P2P_TRACE");
+  if (tr && atoi(tr)) {
+    S2_CUDA(cudaMalloc(&a.trace, sizeof(unsigned long long) * 64 * G), "cudaMalloc(trace)");
+    S2_CUDA(cudaMemset(a.trace, 0, sizeof(unsigned long long) * 64 * G), "cudaMemset(trace)");
+  }
+  plan->fused = false;
+  const char* fz = getenv("S2_FUSED");
+  if (fz && atoi(fz) != 0 && plan->p.block_size == 1 && !a.nvls) {  // opt-in
+    cudaError_t e = s2::xdecode_grid(plan->p.hp, W, a.oneshot, &plan->x_grid);
+    if (e == cudaSuccess && plan->x_grid > 0) plan->fused = true;
+    else cudaGetLastError();
+  }
+  for (int k = 0; k < 2; ++k) {
+    plan->tables[k] = reinterpret_cast<float*>(plan->arena + a.off_table[k]);
+    S2_CUDA(cudaMalloc(&plan->counters[k], sizeof(unsigned long long) * S2_NUM_COUNTERS), "cudaMalloc(counters)");
+    S2_CUDA(cudaMemset(plan->counters[k], 0, sizeof(unsigned long long) * S2_NUM_COUNTERS), "cudaMemset(counters)");
+  }
+  plan->phase = 0;
+  S2_CUDA(cudaDeviceSynchronize(), "p2p init");
+  return S2_OK;
+}
+
+// CUDA-IPC arena: one cudaMalloc per rank, handles exchanged through one ncclAllGather
+static int setup_p2p(s2_plan* plan) {
+  const int W = plan->world;
+  int G = 0;
+  int rc = sm_count(&G);
+  if (rc) return rc;
+  const int64_t off = layout_p2p(plan, W, G);
+  s2::P2PArgs& a = plan->pa;
   S2_CUDA(cudaMalloc(&plan->arena, off), "cudaMalloc(arena)");
   S2_CUDA(cudaMemset(plan->arena, 0, off), "cudaMemset(arena)");
   S2_CUDA(cudaDeviceSynchronize(), "arena init");
+  plan->arena_owned = true;
   struct Rec {
     cudaIpcMemHandle_t h;
     int64_t bytes;
@@ -363,7 +413,7 @@ static int setup_p2p(s2_plan* plan) {
   std::vector<Rec> all(W);
   cudaStream_t st = nullptr;
   S2_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
-  int rc = S2_OK;
+  rc = S2_OK;
   if (cudaMemcpyAsync(d, &rec, sizeof rec, cudaMemcpyHostToDevice, st) != cudaSuccess ||
       ncclAllGather(d, d + sizeof(Rec), sizeof(Rec), ncclUint8, plan->comm, st) != ncclSuccess ||
       cudaMemcpyAsync(all.data(), d + sizeof(Rec), sizeof(Rec) * W, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
@@ -385,34 +435,47 @@ static int setup_p2p(s2_plan* plan) {
     }
     a.base[q] = plan->peer[q];
   }
-  plan->p2p_grid = G;
-  plan->p2p = true;
-  // fused exchange+decode (k_xdecode): cooperative grid = co-resident CTAs (<= 4 per SM)
-  plan->fused = false;
-  const char* fz = getenv("S2_FUSED");
-  if (fz && atoi(fz) != 0 && plan->p.block_size == 1) {  // opt-in: measured slower than separate kernels
-    s2::DecodeCtx probe{};
-    probe.dim = plan->p.dim;
-    probe.bs = 1;
-    cudaError_t e = s2::xdecode_grid(plan->p.hp, W, a.oneshot, &plan->x_grid);
-    if (e == cudaSuccess && plan->x_grid > 0) plan->fused = true;
-    else cudaGetLastError();
+  return finish_p2p(plan, G);
+}
+
+int s2_comm_init_mode(s2_plan* plan, int world, int rank, const void* unique_id, int mode) {
+  if (!plan) return fail(S2_EINVAL, "NULL plan");
+  if (mode < S2_COMM_IPC || mode > S2_COMM_EXTERNAL) return fail(S2_EINVAL, "unknown comm mode %d", mode);
+  plan->comm_mode = mode;
+  return s2_comm_init(plan, world, rank, unique_id);
+}
+
+int64_t s2_p2p_arena_bytes(s2_plan* plan, int world) {
+  if (!plan || world < 2 || world > s2::kMaxWorld) return -1;
+  int G = 0;
+  if (sm_count(&G)) return -1;
+  const int saved = plan->world;
+  plan->world = world;
+  const int64_t b = layout_p2p(plan, world, G);
+  plan->world = saved;
+  return b;
+}
+
+int s2_comm_attach(s2_plan* plan, const uint64_t* bases, int world, uint64_t mc_base) {
+  if (!plan || !bases) return fail(S2_EINVAL, "NULL argument to s2_comm_attach");
+  if (plan->world != world || world < 2) return fail(S2_EINVAL, "attach: world %d does not match the plan", world);
+  if (plan->comm_mode != S2_COMM_EXTERNAL) return fail(S2_EINVAL, "attach needs s2_comm_init_mode(..., S2_COMM_EXTERNAL)");
+  int G = 0;
+  int rc = sm_count(&G);
+  if (rc) return rc;
+  const int64_t bytes = layout_p2p(plan, world, G);
+  s2::P2PArgs& a = plan->pa;
+  for (int q = 0; q < world; ++q) {
+    plan->peer[q] = reinterpret_cast<char*>(bases[q]);
+    a.base[q] = plan->peer[q];
   }
-  a.trace = nullptr;
-  const char* tr = getenv("S2_P2P_TRACE");
-  if (tr && atoi(tr)) {
-    S2_CUDA(cudaMalloc(&a.trace, sizeof(unsigned long long) * 64 * G), "cudaMalloc(trace)");
-    S2_CUDA(cudaMemset(a.trace, 0, sizeof(unsigned long long) * 64 * G), "cudaMemset(trace)");
-  }
-  // the ping-pong tables of s2_reduce live in the arena; counters stay private
-  for (int k = 0; k < 2; ++k) {
-    plan->tables[k] = reinterpret_cast<float*>(plan->arena + a.off_table[k]);
-    S2_CUDA(cudaMalloc(&plan->counters[k], sizeof(unsigned long long) * S2_NUM_COUNTERS), "cudaMalloc(counters)");
-    S2_CUDA(cudaMemset(plan->counters[k], 0, sizeof(unsigned long long) * S2_NUM_COUNTERS), "cudaMemset(counters)");
-  }
-  plan->phase = 0;
-  S2_CUDA(cudaDeviceSynchronize(), "p2p init");
-  return S2_OK;
+  plan->arena = plan->peer[plan->rank];
+  plan->arena_owned = false;
+  a.mc = reinterpret_cast<char*>(mc_base);
+  const char* nv = getenv("S2_NVLS");
+  a.nvls = (mc_base != 0 && !(nv && atoi(nv) == 0)) ? 1 : 0;
+  S2_CUDA(cudaMemset(plan->arena, 0, bytes), "cudaMemset(arena)");
+  return finish_p2p(plan, G);
 }
 
 int s2_comm_init(s2_plan* plan, int world, int rank, const void* unique_id) {
@@ -427,7 +490,8 @@ int s2_comm_init(s2_plan* plan, int world, int rank, const void* unique_id) {
     memcpy(&id, unique_id, sizeof id);
     S2_NCCL(ncclCommInitRank(&plan->comm, world, id, rank), "ncclCommInitRank");
     const char* agg = getenv("S2_AGG");
-    if (!(agg && strcmp(agg, "nccl") == 0)) {
+    const bool nccl_only = (agg && strcmp(agg, "nccl") == 0) || plan->comm_mode == S2_COMM_NCCL;
+    if (!nccl_only && plan->comm_mode != S2_COMM_EXTERNAL) {
       if (world > s2::kMaxWorld) return fail(S2_EINVAL, "peer-memory exchange supports world <= %d", s2::kMaxWorld);
       int rc = setup_p2p(plan);
       if (rc) return rc;
@@ -531,7 +595,8 @@ int s2_reduce(s2_plan* plan, const float* g, float* out, uint64_t* counters, voi
       plan->pa.cur = cur;
       S2_CUDA(s2::launch_p2p_aggregate(plan->pa, plan->p2p_grid, st), "s2_reduce/p2p aggregate");
       un = reinterpret_cast<const uint32_t*>(plan->arena + plan->pa.off_union[cur]);
-      table = reinterpret_cast<float*>(plan->arena + plan->pa.off_tsum[cur]);  // == tables[cur] when two-shot
+      if (!plan->pa.nvls)  // one-shot sums into tsum; two-shot and NVLS reduce into tables[cur] in place
+        table = reinterpret_cast<float*>(plan->arena + plan->pa.off_tsum[cur]);
     } else {
       rc = s2_aggregate(plan, table, bitmap, plan->unionmap, stream);
       if (rc) return rc;

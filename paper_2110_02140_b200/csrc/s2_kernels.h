@@ -56,6 +56,8 @@ struct P2PArgs {
   int world, rank, cur;
   int oneshot;                // 1: one-shot exchange (single barrier), 0: two-shot
   int table_only;             // 1: bitmaps are OR-ed by the decode from peer memory (no bitmap exchange)
+  char* mc;                   // NVLS multicast address of the arena (nullptr: none)
+  int nvls;                   // 1: reduce in the NVSwitch (multimem.ld_reduce / multimem.st)
   unsigned long long* trace;  // optional: per-CTA globaltimer stamps [G][8] (S2_P2P_TRACE=1)
 };
 cudaError_t launch_p2p_aggregate(const P2PArgs& a, int grid, cudaStream_t st);

@@ -256,6 +256,89 @@ __global__ void __launch_bounds__(kP2PThreads) k_p2p_oneshot(const __grid_consta
   S2_TRACE(4);
 }
 
+// ============================================================ NVLS (in-switch) exchange
+//
+// With torch symmetric memory the arena also has a multicast address: a load-reduce on it
+// returns the SUM (float) or OR (bits) of all W ranks' copies, computed inside the
+// NVSwitch, and a multicast store writes all W copies.  Rank r reduces slice r of the
+// table and the bitmap and broadcasts the result into every rank's table[cur] (in place)
+// and union[cur]: per rank (table + bitmap)/W bytes in and out over NVLink, instead of
+// 2(W-1)/W (two-shot) — and no peer ever reads another's partially written slice.
+__device__ __forceinline__ float4 mc_ld_add_v4f32(const void* p) {
+  float4 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void mc_st_v4f32(void* p, float4 v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ uint64_t mc_ld_or_b64(const void* p) {
+  uint64_t v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.or.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void mc_st_b64(void* p, uint64_t v) {
+  asm volatile("multimem.st.relaxed.sys.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+template <int W>
+__global__ void __launch_bounds__(kP2PThreads) k_nvls_exchange(const __grid_constant__ P2PArgs a) {
+  __shared__ uint32_t s_ep;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic launch: compress must be complete
+  S2_TRACE(0);
+  if (threadIdx.x == 0) {
+    uint32_t* e = reinterpret_cast<uint32_t*>(a.base[a.rank] + a.off_epoch) + blockIdx.x;
+    s_ep = *e + 1u;
+    *e = s_ep;
+  }
+  __syncthreads();
+  const uint32_t ep = s_ep;
+  const int me = a.rank, cur = a.cur;
+  const int64_t t4 = a.cells / 4 / W;  // float4 per slice
+  const int64_t w8 = a.words / 2 / W;  // uint64 per slice
+  cross_rank_barrier<W>(a, a.off_flags_a, ep);  // every rank's compress is complete
+  S2_TRACE(1);
+  {
+    int64_t lo, hi;
+    chunk_of(t4 + w8, lo, hi);
+    char* tab = a.mc + a.off_table[cur] + me * t4 * 16;
+    const char* bm = a.mc + a.off_bitmap[cur] + me * w8 * 8;
+    char* un = a.mc + a.off_union[cur] + me * w8 * 8;
+    constexpr int B = 4;  // independent load-reduces in flight per thread
+    for (int64_t i0 = lo + threadIdx.x; i0 < hi; i0 += (int64_t)B * kP2PThreads) {
+      float4 tv[B];
+      uint64_t bv[B];
+#pragma unroll
+      for (int k = 0; k < B; ++k) {
+        const int64_t i = i0 + (int64_t)k * kP2PThreads;
+        if (i < hi) {
+          if (i < t4) tv[k] = mc_ld_add_v4f32(tab + i * 16);
+          else bv[k] = mc_ld_or_b64(bm + (i - t4) * 8);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < B; ++k) {
+        const int64_t i = i0 + (int64_t)k * kP2PThreads;
+        if (i < hi) {
+          if (i < t4) mc_st_v4f32(tab + i * 16, tv[k]);
+          else mc_st_b64(un + (i - t4) * 8, bv[k]);
+        }
+      }
+    }
+  }
+  asm volatile("fence.proxy.alias;" ::: "memory");  // multicast-alias stores before the unicast flag
+  S2_TRACE(2);
+  __syncthreads();
+  if (threadIdx.x < W) __threadfence_system();
+  cross_rank_barrier<W>(a, a.off_flags_b, ep);  // every slice of every rank is broadcast
+  S2_TRACE(3);
+}
+
 // ============================================================ fused exchange + decode
 //
 // k_xdecode replaces k_p2p_* + k_decode for W > 1: one cooperative launch per reduce
@@ -546,7 +629,18 @@ static cudaError_t launch_coop(const void* fn, const P2PArgs& a, int grid, cudaS
 
 cudaError_t launch_p2p_aggregate(const P2PArgs& a, int grid, cudaStream_t st) {
   const void* fn = nullptr;
-  if (a.oneshot) {
+  if (a.nvls) {
+    switch (a.world) {
+      case 2: fn = (const void*)k_nvls_exchange<2>; break;
+      case 3: fn = (const void*)k_nvls_exchange<3>; break;
+      case 4: fn = (const void*)k_nvls_exchange<4>; break;
+      case 5: fn = (const void*)k_nvls_exchange<5>; break;
+      case 6: fn = (const void*)k_nvls_exchange<6>; break;
+      case 7: fn = (const void*)k_nvls_exchange<7>; break;
+      case 8: fn = (const void*)k_nvls_exchange<8>; break;
+      default: return cudaErrorInvalidValue;
+    }
+  } else if (a.oneshot) {
     switch (a.world) {
       case 2: fn = (const void*)k_p2p_oneshot<2>; break;
       case 3: fn = (const void*)k_p2p_oneshot<3>; break;

@@ -65,10 +65,53 @@ class S2Reducer:
             rank = dist.get_rank(group) if world > 1 else 0
         self.world, self.rank = int(world), int(rank)
         uid = (ctypes.c_uint8 * 128)()
+        self._symm = None
+        mode = 0  # S2_COMM_IPC
         if self.world > 1:
             ctypes.memmove(uid, broadcast_unique_id(self.rank, group), 128)
-        check(lib.s2_comm_init(self.plan.handle, self.world, self.rank, uid), "comm init")
+            mode = self._exchange_mode(group)
+        check(lib.s2_comm_init_mode(self.plan.handle, self.world, self.rank, uid, mode), "comm init")
+        if mode == 2:  # S2_COMM_EXTERNAL: torch symmetric memory (+ NVLS multicast address)
+            self._attach_symmetric(group)
         check(lib.s2_comm_check(self.plan.handle, stream_ptr()), "comm check")
+
+    def _exchange_mode(self, group) -> int:
+        """NVLS multicast through torch symmetric memory when the box supports it (S2_NVLS=0 disables),
+        else the CUDA-IPC arena (S2_AGG=nccl: NCCL collectives)."""
+        import os
+
+        if os.environ.get("S2_AGG") == "nccl":
+            return 1
+        if os.environ.get("S2_NVLS", "1") == "0":
+            return 0
+        try:
+            import torch.distributed._symmetric_memory as symm_mem
+
+            ok = bool(symm_mem._SymmetricMemory.has_multicast_support(symm_mem.DeviceType.CUDA,
+                                                                       self.device.index))
+        except Exception:  # noqa: BLE001 - older torch / no NVSwitch: IPC arena
+            ok = False
+        import torch.distributed as dist
+
+        flags = [None] * self.world
+        dist.all_gather_object(flags, ok, group=group)
+        return 2 if all(flags) else 0
+
+    def _attach_symmetric(self, group) -> None:
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+
+        nbytes = int(lib.s2_p2p_arena_bytes(self.plan.handle, self.world))
+        if nbytes <= 0:
+            raise RuntimeError("s2_p2p_arena_bytes failed")
+        buf = symm_mem.empty(nbytes, dtype=torch.uint8, device=self.device)
+        hdl = symm_mem.rendezvous(buf, group if group is not None else dist.group.WORLD)
+        bases = (ctypes.c_uint64 * self.world)(*[int(p) for p in hdl.buffer_ptrs])
+        mc = int(getattr(hdl, "multicast_ptr", 0) or 0)
+        check(lib.s2_comm_attach(self.plan.handle, bases, self.world, mc), "comm attach")
+        self._symm = (buf, hdl)  # keep the mapping alive for the plan's lifetime
+        torch.cuda.synchronize()
+        dist.barrier(group=group)  # every arena is zeroed before any rank signals into it
 
     def reduce(self, g: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         """Averaged gradient estimate: median-of-rows sketch query ÷ world at every union-bitmap
