@@ -76,13 +76,13 @@ class S2Reducer:
         check(lib.s2_comm_check(self.plan.handle, stream_ptr()), "comm check")
 
     def _exchange_mode(self, group) -> int:
-        """NVLS multicast through torch symmetric memory when the box supports it (S2_NVLS=0 disables),
-        else the CUDA-IPC arena (S2_AGG=nccl: NCCL collectives)."""
+        """CUDA-IPC arena by default; S2_NVLS=1 opts into torch symmetric memory + NVLS multicast
+        (measured slower at W = 2 and 4); S2_AGG=nccl uses NCCL collectives."""
         import os
 
         if os.environ.get("S2_AGG") == "nccl":
             return 1
-        if os.environ.get("S2_NVLS", "1") == "0":
+        if os.environ.get("S2_NVLS", "0") == "0":
             return 0
         try:
             import torch.distributed._symmetric_memory as symm_mem
