@@ -99,6 +99,12 @@ int s2_sketch_insert(const s2_plan* plan, const int64_t* idx, const float* vals,
 int s2_sketch_query(const s2_plan* plan, const int64_t* idx, int64_t n, const float* table,
                     float* out, void* stream);
 
+/* block_topk (sparse.py:70-80): flags of the k blocks of largest L2 norm (float64 norms,
+ * ties to the lower block index) into `bitmap`; scratch >= s2_block_topk_scratch_bytes */
+int64_t s2_block_topk_scratch_bytes(const s2_plan* plan);
+int s2_block_topk(const s2_plan* plan, const float* g, int64_t k, uint32_t* bitmap, void* scratch,
+                  void* stream);
+
 /* BlockMask.union over `nmasks` stacked bitmaps (sparse.py:55-58) */
 int s2_bitmap_or(int64_t words, const uint32_t* stacked, int nmasks, uint32_t* out, void* stream);
 

@@ -49,6 +49,8 @@ SIGNATURES = {
     "s2_table_sum": (c_int, [c_int64, c_void_p, c_int, c_void_p, c_void_p]),
     "s2_selected_count": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "s2_compact_scratch_bytes": (c_int64, [c_void_p]),
+    "s2_block_topk_scratch_bytes": (c_int64, [c_void_p]),
+    "s2_block_topk": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
     "s2_compact": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "s2_nccl_unique_id": (c_int, [c_void_p]),
     "s2_comm_init": (c_int, [c_void_p, c_int, c_int, c_void_p]),

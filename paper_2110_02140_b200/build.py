@@ -14,7 +14,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libs2.so")
-SOURCES = ["s2_kernels.cu", "s2_p2p.cu", "s2_capi.cu"]
+SOURCES = ["s2_kernels.cu", "s2_p2p.cu", "s2_topk.cu", "s2_capi.cu"]
 HEADERS = ["s2_common.cuh", "s2_kernels.h", "s2_decode.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -250,6 +250,18 @@ int s2_selected_count(const s2_plan* plan, const uint32_t* bitmap, uint64_t* cou
   return S2_OK;
 }
 
+int64_t s2_block_topk_scratch_bytes(const s2_plan* plan) {
+  return plan ? s2::topk_scratch_bytes(plan->p) : -1;
+}
+
+int s2_block_topk(const s2_plan* plan, const float* g, int64_t k, uint32_t* bitmap, void* scratch, void* stream) {
+  if (!plan || !g || !bitmap || !scratch) return fail(S2_EINVAL, "NULL argument to s2_block_topk");
+  if (k < 1 || k > plan->p.num_blocks)
+    return fail(S2_EINVAL, "k must be in [1, %lld], got %lld", (long long)plan->p.num_blocks, (long long)k);
+  S2_CUDA(s2::launch_block_topk(plan->p, g, k, bitmap, scratch, as_stream(stream)), "s2_block_topk");
+  return S2_OK;
+}
+
 int64_t s2_compact_scratch_bytes(const s2_plan* plan) {
   return plan ? s2::compact_scratch_bytes(plan->p) : -1;
 }

@@ -978,6 +978,11 @@ cudaError_t launch_selected_count(const Plan& p, const uint32_t* bitmap,
   return cudaGetLastError();
 }
 
+cudaError_t launch_exclusive_scan(int64_t* a, int64_t n, int64_t* total, cudaStream_t st) {
+  k_scan<<<1, 1024, 0, st>>>(a, n, total);
+  return cudaGetLastError();
+}
+
 int64_t compact_scratch_bytes(const Plan& p) {
   const int64_t ntiles = (p.dim + kTile - 1) / kTile;
   return (ntiles + 1) * (int64_t)sizeof(int64_t);

@@ -37,6 +37,11 @@ cudaError_t launch_table_sum(int64_t cells, const float* stacked, int ntables, f
 cudaError_t launch_selected_count(const Plan& p, const uint32_t* bitmap,
                                   unsigned long long* counters, cudaStream_t st);
 int64_t compact_scratch_bytes(const Plan& p);
+cudaError_t launch_exclusive_scan(int64_t* a, int64_t n, int64_t* total, cudaStream_t st);
+// block_topk (sparse.py:70-80) into `bitmap`; scratch >= topk_scratch_bytes(p)
+int64_t topk_scratch_bytes(const Plan& p);
+cudaError_t launch_block_topk(const Plan& p, const float* g, int64_t k, uint32_t* bitmap, void* scratch,
+                              cudaStream_t st);
 cudaError_t launch_compact(const Plan& p, const uint32_t* bitmap, const float* g, int64_t* idx_out,
                            float* val_out, int64_t* count, void* scratch, cudaStream_t st);
 

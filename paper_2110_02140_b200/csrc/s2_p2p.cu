@@ -454,7 +454,6 @@ k_xdecode(const __grid_constant__ P2PArgs a, const __grid_constant__ DecodeCtx d
   const int64_t per = (ntiles + G - 1) / G;
   const int64_t tb = (int64_t)blockIdx.x * per < ntiles ? (int64_t)blockIdx.x * per : ntiles;
   const int64_t te = tb + per < ntiles ? tb + per : ntiles;
-  const int64_t nwords = (dc.dim + 31) / 32;
   uint32_t* un = reinterpret_cast<uint32_t*>(a.base[me] + a.off_union[cur]);
   {
     // union words of [tb, te) tiles: 32 words per tile -> 8 uint4 per tile, W loads each (batched)

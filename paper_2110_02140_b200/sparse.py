@@ -141,14 +141,22 @@ def nonzero_mask(g, num_blocks: int | None = None) -> BlockMask:
 
 
 def block_topk(g, num_blocks: int, k: int) -> BlockMask:
-    """Top-k blocks by L2 norm, ties to the lower index (sparse.py:70-80).
+    """Select the k blocks of largest L2 norm, ties to the lower block index (sparse.py:70-80).
 
-    Block Top-K is §8(f) "next" work; it is not on the north-star path, which
-    uses the non-zero mask rule.  Until the GPU kernel lands this raises
-    rather than falling back to the CPU.
-    """
-    raise NotImplementedError("block_topk: the GPU block Top-K kernel is scheduled for a later round "
-                              "(SURVEY.md §8(f) rank 4); use mask=None (non-zero rule)")
+    float64 block norms + an 8-pass radix select with a stable tie-break, on the GPU
+    (csrc/s2_topk.cu)."""
+    g = as_gradient(g)
+    partition = BlockPartition(g.numel(), num_blocks)
+    if not 1 <= k <= num_blocks:
+        raise ValueError(f"k must be in [1, {num_blocks}], got {k}")
+    if not bool(torch.isfinite(g).all()):
+        raise ValueError("gradient vector contains NaN or Inf")  # as_gradient, core.py:157-158
+    plan = get_plan(partition.dim, num_blocks, 1, 1, 0)
+    scratch = torch.empty(int(lib.s2_block_topk_scratch_bytes(plan.handle)) // 8 + 1, dtype=torch.int64,
+                          device=g.device)
+    words = torch.empty(_words_for(num_blocks), dtype=torch.int32, device=g.device)
+    check(lib.s2_block_topk(plan.handle, ptr(g), int(k), ptr(words), ptr(scratch), stream_ptr()), "block_topk")
+    return BlockMask(partition, words=words)
 
 
 def sketch_cols(size_ratio: float, alpha: float, dim: int, rows: int = DEFAULT_ROWS) -> int:
@@ -335,9 +343,8 @@ class SparseSketchCompressor:
     """Block-mask + signed-sketch compressor plugin (sparse.py:288-323).
 
     Same protocol as the reference (mergeable, name, prepare, compress, merge,
-    decompress, payload_nbytes).  ``mask="nonzero"`` selects the north-star
-    non-zero bitmap; ``mask="topk"`` (the reference default) needs the GPU
-    block Top-K.
+    decompress, payload_nbytes).  ``mask="topk"`` (the reference default) runs the
+    GPU block Top-K; ``mask="nonzero"`` selects the north-star non-zero bitmap.
     """
 
     mergeable = True

@@ -342,3 +342,45 @@ def test_host_pipeline(s2):
     for g, go in zip(gs, hout):
         ref = o.decompress(o.compress(g, g != 0, 3, 7919, 3))
         assert np.array_equal(go.numpy(), ref.astype(np.float32))
+
+
+def test_block_topk_golden_and_random(s2):
+    """GPU block_topk (sparse.py:70-80) against the live-reference fixture and the oracle."""
+    z = load("s2_blocks_topk")
+    for w in range(int(z["W"])):
+        m = s2.block_topk(cuda(z["grads"][w]), 333, 40)
+        assert np.array_equal(words_u32(m.words), z["words"][w])
+    rng = np.random.default_rng(8)
+    for d, nb, k in ((10_000, 100, 7), (4097, 4097, 300), (100_000, 5000, 1), (100_000, 5000, 5000),
+                     (1_000_003, 7919, 250), (33, 5, 2)):
+        g = (rng.standard_normal(d) * (rng.random(d) < 0.5)).astype(np.float32)
+        m = s2.block_topk(cuda(g), nb, k)
+        assert np.array_equal(m.flags, o.block_topk(g, nb, k)), (d, nb, k)
+        assert int(m.flags.sum()) == k
+
+
+def test_block_topk_ties_lower_index(s2):
+    """SPEC.md:425 tight case: equal block energies -> ties broken by the lower block index."""
+    g = np.ones(16, np.float32)
+    assert s2.block_topk(cuda(g), 4, 1).flags.tolist() == [True, False, False, False]
+    g = np.tile(np.array([1.0, -2.0], np.float32), 40)
+    assert s2.block_topk(cuda(g), 8, 3).flags.tolist() == [True, True, True] + [False] * 5
+    g = np.zeros(100, np.float32)  # all-zero norms: the first k blocks
+    assert np.array_equal(s2.block_topk(cuda(g), 10, 4).flags, o.block_topk(g, 10, 4))
+    with pytest.raises(ValueError, match=r"k must be in \[1, 10\], got 11"):
+        s2.block_topk(cuda(g), 10, 11)
+
+
+def test_compressor_plugin_topk(s2):
+    """SparseSketchCompressor with the reference's default block Top-K mask vs the oracle."""
+    rng = np.random.default_rng(9)
+    d, nb, k = 50_000, 500, 25
+    comp = s2.SparseSketchCompressor(d, nb, k)
+    g = (rng.integers(-100, 100, d) * (rng.random(d) < 0.3)).astype(np.float32)
+    pay = comp.compress(cuda(g))
+    flags = o.block_topk(g, nb, k)
+    assert np.array_equal(pay.mask.flags, flags)
+    ref = o.compress(g, flags, 3, comp.cols, 0)
+    assert np.array_equal(host(pay.table.table), ref.table.astype(np.float32))
+    assert pay.alpha == ref.alpha
+    assert np.array_equal(host(comp.decompress(comp.merge([pay]))), o.decompress(ref).astype(np.float32))

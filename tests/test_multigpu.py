@@ -17,14 +17,25 @@ def ngpus():
     return torch.cuda.device_count()
 
 
+VARIANTS = {
+    "ipc": {},                                 # default: CUDA-IPC arena, one-shot (W=2) / two-shot (W>2)
+    "ipc_twoshot": {"S2_P2P_ONESHOT_MAXW": "1"},
+    "nvls": {"S2_NVLS": "1"},                  # torch symmetric memory + multimem in-switch reduce
+    "nccl": {"S2_AGG": "nccl"},                # NCCL all-reduce + all-gather + OR kernel
+    "fused": {"S2_FUSED": "1"},                # exchange + decode in one kernel
+}
+
+
+@pytest.mark.parametrize("variant", sorted(VARIANTS))
 @pytest.mark.parametrize("world", [2, 4, 8])
-def test_dist_reduce_parity(world):
+def test_dist_reduce_parity(world, variant):
     if ngpus() < world:
         pytest.skip(f"needs {world} GPUs")
-    port = 29500 + world
+    port = 29500 + world * 10 + sorted(VARIANTS).index(variant)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "tools", "dist_check.py")]
-    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    env = dict(os.environ, **VARIANTS[variant])
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
     line = [x for x in p.stdout.splitlines() if x.startswith("{")][-1]
     rep = json.loads(line)
