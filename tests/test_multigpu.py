@@ -40,3 +40,15 @@ def test_dist_reduce_parity(world, variant):
     line = [x for x in p.stdout.splitlines() if x.startswith("{")][-1]
     rep = json.loads(line)
     assert rep["all_ranks_ok"], rep
+
+
+def test_ddp_comm_hook_trains():
+    """S2 as a DDP comm hook with error feedback (casq.ef_step semantics) on an embedding model."""
+    if ngpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port=29590", os.path.join(ROOT, "tools", "ddp_check.py")]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    rep = json.loads([x for x in p.stdout.splitlines() if x.startswith("{")][-1])
+    assert rep["ok"], rep
