@@ -13,8 +13,6 @@ The bucket's flat gradient is reduced by ``S2Reducer`` (compress -> NVLink excha
 median decode, averaged over ranks) on the current stream; DDP receives the estimate.
 """
 
-from __future__ import annotations
-
 import torch
 import torch.distributed as dist
 
@@ -31,8 +29,8 @@ class S2HookState:
         self.group = process_group
         self.rows, self.size_ratio, self.alpha, self.seed = rows, size_ratio, alpha, seed
         self.error_feedback = error_feedback
-        self.reducers: dict[int, S2Reducer] = {}
-        self.residuals: dict[int, torch.Tensor] = {}
+        self.reducers = {}   # bucket numel -> S2Reducer
+        self.residuals = {}  # bucket index -> error-feedback residual
 
     def reducer(self, numel: int) -> S2Reducer:
         r = self.reducers.get(numel)
@@ -43,7 +41,7 @@ class S2HookState:
         return r
 
 
-def s2_comm_hook(state: S2HookState, bucket: "dist.GradBucket") -> torch.futures.Future:
+def s2_comm_hook(state: S2HookState, bucket: dist.GradBucket) -> torch.futures.Future[torch.Tensor]:
     g = bucket.buffer()
     flat = g.reshape(-1)
     if flat.dtype != torch.float32:
