@@ -38,9 +38,9 @@ class Model(nn.Module):
 model = Model().cuda()
 true_w = torch.randn(V, device="cuda")
 ddp = nn.parallel.DistributedDataParallel(model, device_ids=[rank], bucket_cap_mb=1000)
-state = S2HookState(size_ratio=2.0, alpha=0.02, seed=1)
+state = S2HookState(size_ratio=8.0, alpha=0.03, seed=1)
 ddp.register_comm_hook(state, s2_comm_hook)
-opt = torch.optim.SGD(ddp.parameters(), lr=0.5)
+opt = torch.optim.SGD(ddp.parameters(), lr=0.1)
 g = torch.Generator(device="cuda")
 g.manual_seed(100 + rank)
 losses = []
