@@ -11,6 +11,11 @@ per DDP gradient bucket (``lr`` folded in by the optimizer, so the hook uses 1):
 
 The bucket's flat gradient is reduced by ``S2Reducer`` (compress -> NVLink exchange ->
 median decode, averaged over ranks) on the current stream; DDP receives the estimate.
+
+Error feedback is opt-in (``error_feedback=True``): with W > 1 the residual taken
+against the merged estimate is non-zero wherever ANY rank had a non-zero, so the
+compressed vector densifies step by step and the sketch (sized for alpha) saturates
+unless alpha/size_ratio account for it (measured in tools/ddp_check.py).
 """
 
 import torch
@@ -25,7 +30,7 @@ class S2HookState:
     error-feedback residual per bucket index."""
 
     def __init__(self, process_group=None, rows: int = DEFAULT_ROWS, size_ratio: float = DEFAULT_SIZE_RATIO,
-                 alpha: float = 0.01, seed: int = 0, error_feedback: bool = True):
+                 alpha: float = 0.01, seed: int = 0, error_feedback: bool = False):
         self.group = process_group
         self.rows, self.size_ratio, self.alpha, self.seed = rows, size_ratio, alpha, seed
         self.error_feedback = error_feedback

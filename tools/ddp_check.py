@@ -38,8 +38,22 @@ class Model(nn.Module):
 model = Model().cuda()
 true_w = torch.randn(V, device="cuda")
 ddp = nn.parallel.DistributedDataParallel(model, device_ids=[rank], bucket_cap_mb=1000)
-state = S2HookState(size_ratio=8.0, alpha=0.03, seed=1)
-ddp.register_comm_hook(state, s2_comm_hook)
+state = S2HookState(size_ratio=8.0, alpha=0.03, seed=1, error_feedback=False)
+DIAG = []
+
+
+def diag_hook(st, bucket):
+    exact = bucket.buffer().clone()
+    dist.all_reduce(exact)
+    exact /= world
+    fut = s2_comm_hook(st, bucket)
+    est = bucket.buffer()
+    DIAG.append((float((est - exact).norm() / exact.norm().clamp_min(1e-30)), float(exact.abs().max()),
+                 float(est.abs().max()), int((exact != 0).sum()), int((est != 0).sum())))
+    return fut
+
+
+ddp.register_comm_hook(state, diag_hook)
 opt = torch.optim.SGD(ddp.parameters(), lr=0.1)
 g = torch.Generator(device="cuda")
 g.manual_seed(100 + rank)
@@ -55,7 +69,7 @@ for step in range(150):
 flat = torch.cat([p.grad.reshape(-1) for p in ddp.parameters()])
 h = [None] * world
 dist.all_gather_object(h, flat.double().sum().item())
-rep = {"world": world, "loss_first": float(np.mean(losses[:10])), "loss_last": float(np.mean(losses[-10:])),
+rep = {"diag_first": DIAG[:3], "diag_last": DIAG[-3:], "losses": losses[::15], "world": world, "loss_first": float(np.mean(losses[:10])), "loss_last": float(np.mean(losses[-10:])),
        "grads_replicated": len(set(h)) == 1, "buckets": len(state.reducers)}
 rep["ok"] = rep["grads_replicated"] and rep["loss_last"] < 0.7 * rep["loss_first"]
 if rank == 0:
