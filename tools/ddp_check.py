@@ -39,7 +39,7 @@ def train(hook: bool):
     torch.manual_seed(0)
     model = Model().cuda()
     ddp = nn.parallel.DistributedDataParallel(model, device_ids=[rank], bucket_cap_mb=1000)
-    state = S2HookState(size_ratio=8.0, alpha=0.03, seed=1, error_feedback=False)
+    state = S2HookState(size_ratio=4.0, alpha=0.3, seed=1, error_feedback=False)
     if hook:
         ddp.register_comm_hook(state, diag_hook)
     opt = torch.optim.SGD(ddp.parameters(), lr=2.0)
@@ -79,7 +79,7 @@ dist.all_gather_object(h, flat.double().sum().item())
 rep = {"world": world, "loss_exact_last": float(np.mean(l_exact[-20:])), "loss_s2_last": float(np.mean(l_s2[-20:])),
        "loss_first": float(np.mean(l_s2[:10])), "max_rel_err": max(DIAG), "grads_replicated": len(set(h)) == 1,
        "buckets": len(state.reducers)}
-rep["ok"] = (rep["grads_replicated"] and rep["max_rel_err"] < 0.05
+rep["ok"] = (rep["grads_replicated"] and rep["max_rel_err"] < 0.1
              and rep["loss_s2_last"] <= 1.1 * rep["loss_exact_last"] and rep["loss_s2_last"] < rep["loss_first"])
 if rank == 0:
     print(json.dumps(rep), flush=True)
