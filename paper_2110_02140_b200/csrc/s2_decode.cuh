@@ -111,21 +111,16 @@ __device__ __forceinline__ float finish_value(const DecodeCtx& c, float qv) {
 // buffer is reused once the previous bulk store has finished reading it, and the
 // gathers of the tile's first 32 values overlap that wait.  The ragged last tile
 // uses plain stores.
-// vals: NBUF buffers of kDecTile floats; with NBUF = 2 a tile's bulk store can still be reading
-// one buffer while the next tile is assembled in the other.
-template <int R, bool BLOCKS, int NBUF = 1>
+template <int R, bool BLOCKS>
 __device__ __forceinline__ void decode_range(const DecodeCtx& c, const PeerMaps& pm, int64_t t0, int64_t tstep,
-                                             int64_t tend, const HashParams& hp, uint16_t* q, float* vals_base) {
+                                             int64_t tend, const HashParams& hp, uint16_t* q, float* vals) {
   const int lane = threadIdx.x & 31;
-  int buf = 0;
   const int64_t nelem_words = (c.dim + 31) / 32;
   const int64_t dim = c.dim;
   int64_t t = t0;
   uint32_t wnext = t < tend ? decode_word<BLOCKS>(c.bitmap, pm, t, lane, dim, c.bs, nelem_words) : 0u;
   for (; t < tend; t += tstep) {
     const int64_t base = t * kDecTile;
-    float* vals = vals_base + buf * kDecTile;
-    buf = buf + 1 == NBUF ? 0 : buf + 1;
     const uint32_t word = wnext;
     if (t + tstep < tend) wnext = decode_word<BLOCKS>(c.bitmap, pm, t + tstep, lane, dim, c.bs, nelem_words);
     const int cnt = __popc(word);
@@ -146,10 +141,7 @@ __device__ __forceinline__ void decode_range(const DecodeCtx& c, const PeerMaps&
       pos0 = q[lane];
       v0 = finish_value(c, query_one<R>((uint64_t)(base + pos0), c.table, hp));
     }
-    if (lane == 0) {  // this buffer's previous bulk store has finished reading it
-      if (NBUF == 1) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // vals free again
     __syncwarp();
     const bool full = base + kDecTile <= dim;
     float4* v4 = reinterpret_cast<float4*>(vals);

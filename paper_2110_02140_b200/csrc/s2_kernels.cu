@@ -590,10 +590,8 @@ k_compress_tma(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* _
 
 // zt/zc: the NEXT reduce's sketch table and counters, zeroed here so that the next
 // compress needs no memset (plan ping-pong, s2_reduce); may be null.
-constexpr int kDecWarps = 4;  // 4 warps x (2 x 4 KB value tiles + 2 KB queue) = 40 KB -> 5 CTAs/SM
-
 template <int R, bool BLOCKS>
-__global__ void __launch_bounds__(kDecWarps * 32)
+__global__ void __launch_bounds__(kThreads)
 k_decode(const uint32_t* __restrict__ bitmap, int64_t dim, int64_t bs,
          const float* __restrict__ table, float workers, float inv_workers, int workers_pow2,
          float* __restrict__ out, float4* __restrict__ zt, int64_t zt_n4,
@@ -602,13 +600,13 @@ k_decode(const uint32_t* __restrict__ bitmap, int64_t dim, int64_t bs,
   zero_next(zt, zt_n4, zc);
   griddep_wait();  // bitmap + table come from the compress / exchange kernel
   griddep_launch_dependents();
-  __shared__ uint16_t s_q[kDecWarps][kTile];
-  __shared__ __align__(128) float s_v[kDecWarps][2][kTile];
+  __shared__ uint16_t s_q[kWarps][kTile];
+  __shared__ __align__(16) float s_v[kWarps][kTile];
   const int wib = threadIdx.x >> 5;
   const int64_t ntiles = (dim + kTile - 1) / kTile;
   DecodeCtx c{bitmap, table, out, dim, bs, workers, inv_workers, workers_pow2};
-  decode_range<R, BLOCKS, 2>(c, pm, (int64_t)blockIdx.x * kDecWarps + wib, (int64_t)gridDim.x * kDecWarps, ntiles,
-                             hp, s_q[wib], &s_v[wib][0][0]);
+  decode_range<R, BLOCKS>(c, pm, (int64_t)blockIdx.x * kWarps + wib, (int64_t)gridDim.x * kWarps, ntiles, hp,
+                          s_q[wib], s_v[wib]);
   decode_drain();
 }
 
@@ -921,17 +919,16 @@ template <int R>
 static void launch_decode_r(const Plan& p, const uint32_t* bitmap, const float* table, int workers,
                             float* out, float* zt, unsigned long long* zc, const PeerMaps& pm, cudaStream_t st) {
   const int64_t ntiles = (p.dim + kTile - 1) / kTile;
-  int64_t grid = (ntiles + kDecWarps - 1) / kDecWarps;
-  if (grid > (int64_t)num_sms() * 5) grid = (int64_t)num_sms() * 5;
+  const int grid = grid_for(ntiles, 4);
   const int pow2 = (workers & (workers - 1)) == 0;
   const float inv = 1.0f / (float)workers;
   const int64_t zn4 = zt ? ((int64_t)p.hp.rows * p.hp.cols + 3) / 4 : 0;
   float4* z4 = reinterpret_cast<float4*>(zt);
   if (p.block_size == 1)
-    launch_ex(k_decode<R, false>, (int)grid, kDecWarps * 32, 0, st, bitmap, p.dim, (int64_t)1, table, (float)workers, inv, pow2,
+    launch_ex(k_decode<R, false>, grid, kThreads, 0, st, bitmap, p.dim, (int64_t)1, table, (float)workers, inv, pow2,
               out, z4, zn4, zc, p.hp, pm);
   else
-    launch_ex(k_decode<R, true>, (int)grid, kDecWarps * 32, 0, st, bitmap, p.dim, p.block_size, table, (float)workers, inv,
+    launch_ex(k_decode<R, true>, grid, kThreads, 0, st, bitmap, p.dim, p.block_size, table, (float)workers, inv,
               pow2, out, z4, zn4, zc, p.hp, pm);
 }
 
