@@ -98,19 +98,10 @@ __device__ __forceinline__ void zero_next(float4* __restrict__ zt, int64_t zt_n4
   if (zc != nullptr && blockIdx.x == 0 && threadIdx.x < S2_NUM_COUNTERS) zc[threadIdx.x] = 0ull;
 }
 
-__device__ __forceinline__ float finish_value(const DecodeCtx& c, float qv) {
-  // IEEE division: sparse.py:213 divides the float64 query by workers; x*2^-k is exact
-  return c.workers_pow2 ? qv * c.inv_workers : __fdiv_rn(qv, c.workers);
-}
-
 // Decode warp tiles t0, t0+tstep, ... < tend (one warp).  Per tile: the bitmap word is
-// prefetched one tile ahead and set positions are compacted by a warp scan into q.  A
-// full tile is assembled in shared memory (zero-fill + the decoded values: r gathers,
-// lower median, /W) and written to HBM by ONE TMA bulk store (cp.async.bulk
-// shared->global, `UBLKCP` in SASS) — no per-lane stores, no L1 store traffic; the
-// buffer is reused once the previous bulk store has finished reading it, and the
-// gathers of the tile's first 32 values overlap that wait.  The ragged last tile
-// uses plain stores.
+// prefetched one tile ahead, set positions are compacted by a warp scan into q, values
+// (r gathers + lower median + IEEE /W) land in vals, and the tile is written as dense
+// float4 streaming stores (zeros included).
 template <int R, bool BLOCKS>
 __device__ __forceinline__ void decode_range(const DecodeCtx& c, const PeerMaps& pm, int64_t t0, int64_t tstep,
                                              int64_t tend, const HashParams& hp, uint16_t* q, float* vals) {
@@ -134,59 +125,38 @@ __device__ __forceinline__ void decode_range(const DecodeCtx& c, const PeerMaps&
     pre -= cnt;
     for (uint32_t w = word; w; w &= w - 1u) q[pre++] = (uint16_t)(lane * 32 + (__ffs(w) - 1));
     __syncwarp();
-    // first batch of values into registers (their gathers overlap the buffer wait below)
-    int pos0 = -1;
-    float v0 = 0.f;
-    if (lane < total) {
-      pos0 = q[lane];
-      v0 = finish_value(c, query_one<R>((uint64_t)(base + pos0), c.table, hp));
+    for (int s = lane; s < total; s += 32) {
+      const int pos = q[s];
+      // IEEE division: sparse.py:213 divides the float64 query by workers; x*2^-k is exact
+      const float qv = query_one<R>((uint64_t)(base + pos), c.table, hp);
+      vals[pos] = c.workers_pow2 ? qv * c.inv_workers : __fdiv_rn(qv, c.workers);
     }
-    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // vals free again
     __syncwarp();
     const bool full = base + kDecTile <= dim;
-    float4* v4 = reinterpret_cast<float4*>(vals);
-    if (full) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) v4[k * 32 + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
-      __syncwarp();
-    }
-    if (pos0 >= 0) vals[pos0] = v0;
-    for (int s = 32 + lane; s < total; s += 32) {
-      const int pos = q[s];
-      vals[pos] = finish_value(c, query_one<R>((uint64_t)(base + pos), c.table, hp));
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t wk = __shfl_sync(kFull, word, 4 * k + (lane >> 3));
+      const uint32_t nib = (wk >> ((lane & 7) * 4)) & 0xFu;
+      float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (nib) {
+        const float4 sv = *reinterpret_cast<const float4*>(vals + k * 128 + lane * 4);
+        o.x = (nib & 1u) ? sv.x : 0.f;
+        o.y = (nib & 2u) ? sv.y : 0.f;
+        o.z = (nib & 4u) ? sv.z : 0.f;
+        o.w = (nib & 8u) ? sv.w : 0.f;
+      }
+      const int64_t e = base + k * 128 + lane * 4;
+      if (full) {
+        __stcs(reinterpret_cast<float4*>(c.out + e), o);
+      } else {
+        if (e + 0 < dim) c.out[e + 0] = o.x;
+        if (e + 1 < dim) c.out[e + 1] = o.y;
+        if (e + 2 < dim) c.out[e + 2] = o.z;
+        if (e + 3 < dim) c.out[e + 3] = o.w;
+      }
     }
     __syncwarp();
-    if (full) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
-      __syncwarp();
-      if (lane == 0) {
-        asm volatile(
-            "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n\t"
-            "cp.async.bulk.commit_group;" ::"l"(c.out + base),
-            "r"((uint32_t)__cvta_generic_to_shared(vals)), "r"((uint32_t)(kDecTile * 4))
-            : "memory");
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const uint32_t wk = __shfl_sync(kFull, word, 4 * k + (lane >> 3));
-        const uint32_t nib = (wk >> ((lane & 7) * 4)) & 0xFu;
-        const float4 sv = v4[k * 32 + lane];
-        const int64_t e = base + k * 128 + lane * 4;
-        if (e + 0 < dim) c.out[e + 0] = (nib & 1u) ? sv.x : 0.f;
-        if (e + 1 < dim) c.out[e + 1] = (nib & 2u) ? sv.y : 0.f;
-        if (e + 2 < dim) c.out[e + 2] = (nib & 4u) ? sv.z : 0.f;
-        if (e + 3 < dim) c.out[e + 3] = (nib & 8u) ? sv.w : 0.f;
-      }
-      __syncwarp();
-    }
   }
-}
-
-// the warp's bulk stores must have completed before its results are consumed / smem is freed
-__device__ __forceinline__ void decode_drain() {
-  if ((threadIdx.x & 31) == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-  __syncwarp();
 }
 
 }  // namespace s2

@@ -607,7 +607,6 @@ k_decode(const uint32_t* __restrict__ bitmap, int64_t dim, int64_t bs,
   DecodeCtx c{bitmap, table, out, dim, bs, workers, inv_workers, workers_pow2};
   decode_range<R, BLOCKS>(c, pm, (int64_t)blockIdx.x * kWarps + wib, (int64_t)gridDim.x * kWarps, ntiles, hp,
                           s_q[wib], s_v[wib]);
-  decode_drain();
 }
 
 // ----------------------------------------------------------- bitmap OR (K3b)

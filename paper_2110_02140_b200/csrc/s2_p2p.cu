@@ -553,7 +553,6 @@ k_xdecode(const __grid_constant__ P2PArgs a, const __grid_constant__ DecodeCtx d
     if (t >= te) break;
     decode_range<R, false>(c, none, t, 1, t + 1, hp, s_q[wib], s_v[wib]);
   }
-  decode_drain();
   S2_TRACE(4);
 }
 
