@@ -44,6 +44,9 @@ CONFIGS = {
     "gpt2m_90": dict(dim=355_000_000, alpha=0.10, rows=3, cols=1_048_576, label="GPT-2-medium 355M, 90% sparse"),
     "gpt2m_99": dict(dim=355_000_000, alpha=0.01, rows=3, cols=1_048_576, label="GPT-2-medium 355M, 99% sparse"),
     "gpt2m_999": dict(dim=355_000_000, alpha=0.001, rows=3, cols=262_144, label="GPT-2-medium 355M, 99.9% sparse"),
+    # union densities a W=2 / W=4 reduce decodes (dev configs for single-GPU decode tuning)
+    "resnet50_d2": dict(dim=25_600_000, alpha=0.02, rows=3, cols=262_144, label="ResNet-50-sized, 98% sparse"),
+    "resnet50_d4": dict(dim=25_600_000, alpha=0.04, rows=3, cols=262_144, label="ResNet-50-sized, 96% sparse"),
     "oracle1m": dict(dim=1_000_000, alpha=0.01, rows=3, cols=16_384, label="1M fp32, 99% sparse (configs[0])"),
 }
 N_ROTATE = 4  # distinct gradient buffers cycled through: N_ROTATE * 4d bytes > 126 MB L2
