@@ -125,16 +125,11 @@ __device__ __forceinline__ void decode_range(const DecodeCtx& c, const PeerMaps&
     pre -= cnt;
     for (uint32_t w = word; w; w &= w - 1u) q[pre++] = (uint16_t)(lane * 32 + (__ffs(w) - 1));
     __syncwarp();
-    // two positions per lane per round so two batches' gathers are in flight together
-    for (int s = lane; s < total; s += 64) {
-      const int pos0 = q[s];
-      const bool two = s + 32 < total;
-      const int pos1 = two ? q[s + 32] : pos0;
-      const float q0 = query_one<R>((uint64_t)(base + pos0), c.table, hp);
-      const float q1 = query_one<R>((uint64_t)(base + pos1), c.table, hp);
+    for (int s = lane; s < total; s += 32) {
+      const int pos = q[s];
       // IEEE division: sparse.py:213 divides the float64 query by workers; x*2^-k is exact
-      vals[pos0] = c.workers_pow2 ? q0 * c.inv_workers : __fdiv_rn(q0, c.workers);
-      if (two) vals[pos1] = c.workers_pow2 ? q1 * c.inv_workers : __fdiv_rn(q1, c.workers);
+      const float qv = query_one<R>((uint64_t)(base + pos), c.table, hp);
+      vals[pos] = c.workers_pow2 ? qv * c.inv_workers : __fdiv_rn(qv, c.workers);
     }
     __syncwarp();
     const bool full = base + kDecTile <= dim;
