@@ -844,7 +844,12 @@ template <int R, int LOAD>
 static void launch_compress_rm(const Plan& p, const float* g, uint32_t* bitmap, float* table,
                                unsigned long long* counters, int mode, cudaStream_t st) {
   const int64_t ntiles = (p.dim + kTile - 1) / kTile;
-  const int grid = grid_for(ntiles, LOAD == 0 ? 2 : 4);
+  static int waves = -1;  // S2_COMPRESS_CTAS_PER_SM: grid = SMs x this (>= resident -> extra waves)
+  if (waves < 0) {
+    const char* e = getenv("S2_COMPRESS_CTAS_PER_SM");
+    waves = e ? atoi(e) : 0;
+  }
+  const int grid = grid_for(ntiles, waves > 0 ? waves : (LOAD == 0 ? 2 : 4));
   if (mode == S2_MASK_GIVEN) {
     launch_ex(k_compress<R, 2, LOAD>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table, counters, p.hp);
   } else if (p.block_size == 1) {

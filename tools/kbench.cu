@@ -150,3 +150,55 @@ extern "C" int kb_tma_read(const float* g, int64_t n, uint32_t* out, int stages,
   cudaError_t e = cudaLaunchKernel(fn, dim3(sms * ctas_per_sm), dim3(warps * 32), args, smem, s);
   return (int)e;
 }
+
+// ---- cp.async (LDGSTS) per-warp ring streaming read ----
+template <int STAGES>
+__global__ void k_cpasync_read(const float* __restrict__ g, int64_t n, uint32_t* __restrict__ out) {
+  extern __shared__ __align__(128) unsigned char s_raw[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  float4* ring = reinterpret_cast<float4*>(s_raw) + (size_t)wib * STAGES * 256;
+  const int64_t ntiles = n / 1024;
+  const int64_t nw = (int64_t)gridDim.x * nwarps;
+  int64_t t = (int64_t)blockIdx.x * nwarps + wib;
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  auto issue = [&](int64_t tt, int s) {
+    if (tt < ntiles) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(ring + s * 256 + k * 32 + lane);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(g4 + tt * 256 + k * 32 + lane) : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  for (int s = 0; s < STAGES - 1; ++s) issue(t + s * nw, s);
+  uint32_t acc = 0;
+  int stage = 0;
+  for (; t < ntiles; t += nw) {
+    issue(t + (STAGES - 1) * nw, (stage + STAGES - 1) % STAGES);
+    asm volatile("cp.async.wait_group %0;" ::"n"(STAGES - 1) : "memory");
+    __syncwarp();
+    const float4* tile = ring + stage * 256;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float4 x = tile[k * 32 + lane];
+      acc ^= __float_as_uint(x.x) ^ __float_as_uint(x.w);
+    }
+    __syncwarp();
+    stage = stage + 1 == STAGES ? 0 : stage + 1;
+  }
+  if (acc == 0x12345678u) out[0] = acc;
+}
+
+extern "C" int kb_cpasync_read(const float* g, int64_t n, uint32_t* out, int stages, int warps, int ctas_per_sm,
+                               int sms, void* st) {
+  const int smem = warps * stages * 4096;
+  const void* fn = nullptr;
+  if (stages == 2) fn = (const void*)k_cpasync_read<2>;
+  if (stages == 3) fn = (const void*)k_cpasync_read<3>;
+  if (stages == 4) fn = (const void*)k_cpasync_read<4>;
+  if (!fn) return -1;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  void* args[] = {&g, &n, &out};
+  return (int)cudaLaunchKernel(fn, dim3(sms * ctas_per_sm), dim3(warps * 32), args, smem, (cudaStream_t)st);
+}
