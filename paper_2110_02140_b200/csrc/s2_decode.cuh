@@ -102,60 +102,109 @@ __device__ __forceinline__ void zero_next(float4* __restrict__ zt, int64_t zt_n4
 // prefetched one tile ahead, set positions are compacted by a warp scan into q, values
 // (r gathers + lower median + IEEE /W) land in vals, and the tile is written as dense
 // float4 streaming stores (zeros included).
+// Decode one warp tile (1024 elements at `base`) given its 32 union words (one per lane):
+// set positions are compacted by a warp scan into q, values (r gathers + lower median +
+// IEEE /W) land in vals, and the tile is written as dense float4 streaming stores.
+template <int R>
+__device__ __forceinline__ void decode_tile(const DecodeCtx& c, int64_t base, uint32_t word, const HashParams& hp,
+                                            uint16_t* q, float* vals) {
+  const int lane = threadIdx.x & 31;
+  const int64_t dim = c.dim;
+  const int cnt = __popc(word);
+  int pre = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int n = __shfl_up_sync(kFull, pre, o);
+    if (lane >= o) pre += n;
+  }
+  const int total = __shfl_sync(kFull, pre, 31);
+  pre -= cnt;
+  for (uint32_t w = word; w; w &= w - 1u) q[pre++] = (uint16_t)(lane * 32 + (__ffs(w) - 1));
+  __syncwarp();
+  for (int s = lane; s < total; s += 32) {
+    const int pos = q[s];
+    // IEEE division: sparse.py:213 divides the float64 query by workers; x*2^-k is exact
+    const float qv = query_one<R>((uint64_t)(base + pos), c.table, hp);
+    vals[pos] = c.workers_pow2 ? qv * c.inv_workers : __fdiv_rn(qv, c.workers);
+  }
+  __syncwarp();
+  const bool full = base + kDecTile <= dim;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t wk = __shfl_sync(kFull, word, 4 * k + (lane >> 3));
+    const uint32_t nib = (wk >> ((lane & 7) * 4)) & 0xFu;
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (nib) {
+      const float4 sv = *reinterpret_cast<const float4*>(vals + k * 128 + lane * 4);
+      o.x = (nib & 1u) ? sv.x : 0.f;
+      o.y = (nib & 2u) ? sv.y : 0.f;
+      o.z = (nib & 4u) ? sv.z : 0.f;
+      o.w = (nib & 8u) ? sv.w : 0.f;
+    }
+    const int64_t e = base + k * 128 + lane * 4;
+    if (full) {
+      __stcs(reinterpret_cast<float4*>(c.out + e), o);
+    } else {
+      if (e + 0 < dim) c.out[e + 0] = o.x;
+      if (e + 1 < dim) c.out[e + 1] = o.y;
+      if (e + 2 < dim) c.out[e + 2] = o.z;
+      if (e + 3 < dim) c.out[e + 3] = o.w;
+    }
+  }
+  __syncwarp();
+}
+
+// Decode warp tiles t0, t0+tstep, ... < tend (one warp); the bitmap word is prefetched one
+// tile ahead.
 template <int R, bool BLOCKS>
 __device__ __forceinline__ void decode_range(const DecodeCtx& c, const PeerMaps& pm, int64_t t0, int64_t tstep,
                                              int64_t tend, const HashParams& hp, uint16_t* q, float* vals) {
   const int lane = threadIdx.x & 31;
   const int64_t nelem_words = (c.dim + 31) / 32;
-  const int64_t dim = c.dim;
   int64_t t = t0;
-  uint32_t wnext = t < tend ? decode_word<BLOCKS>(c.bitmap, pm, t, lane, dim, c.bs, nelem_words) : 0u;
+  uint32_t wnext = t < tend ? decode_word<BLOCKS>(c.bitmap, pm, t, lane, c.dim, c.bs, nelem_words) : 0u;
   for (; t < tend; t += tstep) {
-    const int64_t base = t * kDecTile;
     const uint32_t word = wnext;
-    if (t + tstep < tend) wnext = decode_word<BLOCKS>(c.bitmap, pm, t + tstep, lane, dim, c.bs, nelem_words);
-    const int cnt = __popc(word);
-    int pre = cnt;
+    if (t + tstep < tend) wnext = decode_word<BLOCKS>(c.bitmap, pm, t + tstep, lane, c.dim, c.bs, nelem_words);
+    decode_tile<R>(c, t * kDecTile, word, hp, q, vals);
+  }
+}
+
+// Union words OR-ed straight from the W ranks' bitmaps in peer memory (NVLink), fetched
+// kAhead tiles ahead of the decode so the remote latency hides under kAhead tiles of work
+// (the exchange kernel then moves only the sketch table).
+template <int R>
+__device__ __forceinline__ void decode_range_peers(const DecodeCtx& c, const PeerMaps& pm, int64_t t0, int64_t tstep,
+                                                   int64_t tend, const HashParams& hp, uint16_t* q, float* vals) {
+  constexpr int kAhead = 8;
+  const int lane = threadIdx.x & 31;
+  const int64_t nelem_words = (c.dim + 31) / 32;
+  auto fetch = [&](int64_t t) -> uint32_t {
+    uint32_t w = 0;
+    const int64_t wi = t * 32 + lane;
+    if (t < tend && wi < nelem_words) {
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int n = __shfl_up_sync(kFull, pre, o);
-      if (lane >= o) pre += n;
+      for (int r = 0; r < kMaxWorld; ++r)
+        if (r < pm.n) w |= __ldcg(pm.p[r] + wi);
     }
-    const int total = __shfl_sync(kFull, pre, 31);
-    pre -= cnt;
-    for (uint32_t w = word; w; w &= w - 1u) q[pre++] = (uint16_t)(lane * 32 + (__ffs(w) - 1));
-    __syncwarp();
-    for (int s = lane; s < total; s += 32) {
-      const int pos = q[s];
-      // IEEE division: sparse.py:213 divides the float64 query by workers; x*2^-k is exact
-      const float qv = query_one<R>((uint64_t)(base + pos), c.table, hp);
-      vals[pos] = c.workers_pow2 ? qv * c.inv_workers : __fdiv_rn(qv, c.workers);
-    }
-    __syncwarp();
-    const bool full = base + kDecTile <= dim;
+    const int64_t e0 = t * kDecTile + 32 * lane;
+    if (e0 + 32 > c.dim) w &= e0 >= c.dim ? 0u : range_mask(0, (int)(c.dim - e0));
+    return w;
+  };
+  uint32_t cur[kAhead];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const uint32_t wk = __shfl_sync(kFull, word, 4 * k + (lane >> 3));
-      const uint32_t nib = (wk >> ((lane & 7) * 4)) & 0xFu;
-      float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (nib) {
-        const float4 sv = *reinterpret_cast<const float4*>(vals + k * 128 + lane * 4);
-        o.x = (nib & 1u) ? sv.x : 0.f;
-        o.y = (nib & 2u) ? sv.y : 0.f;
-        o.z = (nib & 4u) ? sv.z : 0.f;
-        o.w = (nib & 8u) ? sv.w : 0.f;
-      }
-      const int64_t e = base + k * 128 + lane * 4;
-      if (full) {
-        __stcs(reinterpret_cast<float4*>(c.out + e), o);
-      } else {
-        if (e + 0 < dim) c.out[e + 0] = o.x;
-        if (e + 1 < dim) c.out[e + 1] = o.y;
-        if (e + 2 < dim) c.out[e + 2] = o.z;
-        if (e + 3 < dim) c.out[e + 3] = o.w;
-      }
+  for (int k = 0; k < kAhead; ++k) cur[k] = fetch(t0 + (int64_t)k * tstep);
+  for (int64_t g = t0; g < tend; g += (int64_t)kAhead * tstep) {
+    uint32_t nxt[kAhead];
+#pragma unroll
+    for (int k = 0; k < kAhead; ++k) nxt[k] = fetch(g + (int64_t)(kAhead + k) * tstep);
+#pragma unroll
+    for (int k = 0; k < kAhead; ++k) {
+      const int64_t t = g + (int64_t)k * tstep;
+      if (t < tend) decode_tile<R>(c, t * kDecTile, cur[k], hp, q, vals);
     }
-    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < kAhead; ++k) cur[k] = nxt[k];
   }
 }
 

@@ -23,6 +23,7 @@ VARIANTS = {
     "nvls": {"S2_NVLS": "1"},                  # torch symmetric memory + multimem in-switch reduce
     "nccl": {"S2_AGG": "nccl"},                # NCCL all-reduce + all-gather + OR kernel
     "fused": {"S2_FUSED": "1"},                # exchange + decode in one kernel
+    "bitmap_in_decode": {"S2_P2P_BITMAP_IN_DECODE_MAXW": "8"},  # decode ORs peer bitmaps over NVLink
 }
 
 
