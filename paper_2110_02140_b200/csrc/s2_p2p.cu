@@ -183,6 +183,9 @@ __global__ void __launch_bounds__(kP2PThreads) k_p2p_aggregate(const __grid_cons
   chunk_of(t4 + w4, lo, hi);
   cross_rank_barrier<W>(a, a.off_flags_a, ep);
   S2_TRACE(1);
+  // peers are all in this reduce now: the decode may launch (its prologue zeroes the NEXT
+  // ping-pong table, which no peer reads any more)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   for (int64_t i0 = lo + threadIdx.x; i0 < hi; i0 += (int64_t)p2p_batch<W>() * kP2PThreads)
     reduce_batch<W>(a, i0, hi, t4, w4);  // phase A: reduce-scatter
   S2_TRACE(2);
@@ -214,6 +217,7 @@ __global__ void __launch_bounds__(kP2PThreads) k_p2p_oneshot(const __grid_consta
   chunk_of(t4 + w4, lo, hi);
   cross_rank_barrier<W>(a, a.off_flags_a, s_ep);
   S2_TRACE(1);
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   constexpr int B = p2p_batch<W>();
   for (int64_t i0 = lo + threadIdx.x; i0 < hi; i0 += (int64_t)B * kP2PThreads) {
     uint4 v[B][W];
@@ -303,6 +307,7 @@ __global__ void __launch_bounds__(kP2PThreads) k_nvls_exchange(const __grid_cons
   const int64_t w8 = a.words / 2 / W;  // uint64 per slice
   cross_rank_barrier<W>(a, a.off_flags_a, ep);  // every rank's compress is complete
   S2_TRACE(1);
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   {
     int64_t lo, hi;
     chunk_of(t4 + w8, lo, hi);
