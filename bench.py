@@ -354,6 +354,7 @@ def ours(args, cfg):
     clk = clocks.stop()
 
     red.check_finite()
+    red.check_exchange()
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()

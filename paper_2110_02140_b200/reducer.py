@@ -139,6 +139,13 @@ class S2Reducer:
     def last_nnz(self) -> int:
         return self.counters()[S2_CNT_NNZ]
 
+    def check_exchange(self) -> None:
+        """Raise if a cross-rank barrier of the peer-memory exchange timed out (a rank died or the
+        ranks' reduce sequences diverged); synchronises the device."""
+        torch.cuda.synchronize(self.device)
+        if lib.s2_p2p_error(self.plan.handle):
+            raise RuntimeError("S2 exchange: a cross-rank barrier timed out after 10 s")
+
 
 class HostPipeline:
     """Reduce gradients that live in (pinned) host memory, overlapping PCIe with the GPU.
