@@ -199,3 +199,39 @@ class HostPipeline:
         for e in self.out_done:
             if e is not None:
                 e.synchronize()
+
+
+class GraphedReduce:
+    """CUDA-graph replay of ``S2Reducer.reduce`` on static buffers (no per-step launch cost).
+
+    The plan's sketch tables and counters ping-pong between consecutive reduces, so two
+    graphs are captured — one per phase — and ``__call__`` replays the one matching the
+    plan's current phase.  Do not interleave direct ``reduce`` calls on the same reducer
+    with replays (they flip the phase too; an even number of them is harmless).
+
+        gr = GraphedReduce(reducer, g_static, out_static)
+        g_static.copy_(grad); gr(); use(out_static)
+    """
+
+    def __init__(self, reducer: S2Reducer, g_static: torch.Tensor, out_static: torch.Tensor):
+        self.r, self.g, self.out = reducer, g_static, out_static
+        s = torch.cuda.Stream(device=reducer.device)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(2):  # warm-up: scratch allocated, both phases exercised
+                reducer.reduce(g_static, out=out_static, stream=s)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        self.graphs = []
+        for _ in range(2):
+            gph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gph):
+                reducer.reduce(g_static, out=out_static)
+            self.graphs.append(gph)
+        # capture flipped the phase twice: back at the phase graph 0 was recorded in
+        self.k = 0
+
+    def __call__(self) -> torch.Tensor:
+        self.graphs[self.k].replay()
+        self.k ^= 1
+        return self.out

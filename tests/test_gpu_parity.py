@@ -384,3 +384,22 @@ def test_compressor_plugin_topk(s2):
     assert np.array_equal(host(pay.table.table), ref.table.astype(np.float32))
     assert pay.alpha == ref.alpha
     assert np.array_equal(host(comp.decompress(comp.merge([pay]))), o.decompress(ref).astype(np.float32))
+
+
+def test_graphed_reduce(s2):
+    """CUDA-graph replay (two captured phases) gives the same results as direct reduces."""
+    import torch
+
+    from paper_2110_02140_b200.reducer import GraphedReduce
+
+    d = 1_000_000
+    red = s2.S2Reducer(d, rows=3, cols=16384, seed=0)
+    g_static = torch.zeros(d, device="cuda")
+    out_static = torch.empty(d, device="cuda")
+    gr = GraphedReduce(red, g_static, out_static)
+    for k, alpha in enumerate((0.01, 0.03, 0.002, 0.02, 0.01)):
+        g = o.synthetic_gradient(d, alpha, 10 + k, kind="int")
+        g_static.copy_(torch.from_numpy(g))
+        gr()
+        ref = o.decompress(o.compress(g, g != 0, 3, 16384, 0))
+        assert np.array_equal(host(out_static), ref.astype(np.float32)), k
