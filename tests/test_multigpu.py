@@ -24,6 +24,7 @@ VARIANTS = {
     "nccl": {"S2_AGG": "nccl"},                # NCCL all-reduce + all-gather + OR kernel
     "fused": {"S2_FUSED": "1"},                # exchange + decode in one kernel
     "bitmap_in_decode": {"S2_P2P_BITMAP_IN_DECODE_MAXW": "8"},  # decode ORs peer bitmaps over NVLink
+    "graph": {"S2_CHECK_GRAPH": "1"},          # CUDA-graph replay of the whole reduce
 }
 
 

@@ -37,11 +37,22 @@ dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 import paper_2110_02140_b200 as s2  # noqa: E402
 
 red = s2.S2Reducer(a.dim, rows=a.rows, cols=a.cols, seed=0)
-report = {"world": world, "dim": a.dim}
+graphed = None
+if os.environ.get("S2_CHECK_GRAPH") == "1":  # replay captured CUDA graphs instead of direct calls
+    from paper_2110_02140_b200.reducer import GraphedReduce
+
+    g_static = torch.zeros(a.dim, device="cuda")
+    out_static = torch.empty(a.dim, device="cuda")
+    graphed = GraphedReduce(red, g_static, out_static)
+report = {"world": world, "dim": a.dim, "graph": graphed is not None}
 for kind in ("int", "normal"):
     grads = [o.synthetic_gradient(a.dim, a.alpha, r, kind=kind) for r in range(world)]
     for rep in range(2):  # twice: exercises the ping-pong tables
-        out = red.reduce(torch.from_numpy(grads[rank]).cuda()).cpu().numpy()
+        if graphed is None:
+            out = red.reduce(torch.from_numpy(grads[rank]).cuda()).cpu().numpy()
+        else:
+            g_static.copy_(torch.from_numpy(grads[rank]))
+            out = graphed().cpu().numpy()
     ps = [o.compress(g, g != 0, a.rows, a.cols, 0) for g in grads]
     m = o.merge(ps)
     ref = o.decompress(m)
