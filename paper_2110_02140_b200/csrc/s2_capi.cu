@@ -41,6 +41,8 @@ struct s2_plan {
   bool fused = false;  // W > 1: one k_xdecode launch replaces exchange + decode
   int x_grid = 0;
   int comm_mode = 0;         // S2_COMM_IPC | S2_COMM_NCCL | S2_COMM_EXTERNAL
+  void* list = nullptr;      // split compress: (index, value) list, dim x 8 B (lazy)
+  int split = -1;            // -1: decide from S2_COMPRESS_SPLIT
   bool arena_owned = false;  // cudaMalloc'd here (IPC) vs attached symmetric memory
 };
 
@@ -199,6 +201,7 @@ static void free_p2p(s2_plan* p) {
 
 void s2_plan_destroy(s2_plan* plan) {
   if (!plan) return;
+  cudaFree(plan->list);
   free_p2p(plan);
   if (plan->comm) ncclCommDestroy(plan->comm);
   free_scratch(plan);
@@ -209,6 +212,21 @@ int64_t s2_plan_bitmap_words(const s2_plan* plan) { return plan ? plan->p.words 
 int64_t s2_plan_block_size(const s2_plan* plan) { return plan ? plan->p.block_size : -1; }
 int s2_plan_world(const s2_plan* plan) { return plan ? plan->world : -1; }
 
+static void* split_list(const s2_plan* cplan) {
+  s2_plan* plan = const_cast<s2_plan*>(cplan);  // lazily allocated scratch, not observable state
+  if (plan->split < 0) {
+    const char* e = getenv("S2_COMPRESS_SPLIT");
+    plan->split = e ? atoi(e) : 1;
+  }
+  if (!plan->split || plan->p.block_size != 1) return nullptr;
+  if (!plan->list && cudaMalloc(&plan->list, sizeof(uint64_t) * (size_t)plan->p.dim) != cudaSuccess) {
+    cudaGetLastError();
+    plan->split = 0;
+    return nullptr;
+  }
+  return plan->list;
+}
+
 int s2_compress(const s2_plan* plan, const float* g, uint32_t* bitmap, float* table, int mask_mode,
                 uint64_t* counters, void* stream) {
   if (!plan || !g || !bitmap || !table || !counters) return fail(S2_EINVAL, "NULL argument to s2_compress");
@@ -216,7 +234,7 @@ int s2_compress(const s2_plan* plan, const float* g, uint32_t* bitmap, float* ta
     return fail(S2_EINVAL, "unknown mask mode %d", mask_mode);
   if (reinterpret_cast<uintptr_t>(g) & 15) return fail(S2_EINVAL, "gradient must be 16-byte aligned");
   S2_CUDA(s2::launch_compress(plan->p, g, bitmap, table, reinterpret_cast<unsigned long long*>(counters),
-                              mask_mode, as_stream(stream)),
+                              mask_mode, as_stream(stream), false, split_list(plan)),
           "s2_compress");
   return S2_OK;
 }
@@ -580,7 +598,8 @@ int s2_reduce(s2_plan* plan, const float* g, float* out, uint64_t* counters, voi
   // caller counters: zeroed by memset; plan counters: zeroed by the previous decode
   unsigned long long* cnt = counters ? reinterpret_cast<unsigned long long*>(counters) : plan->counters[cur];
   if (plan->ev[0]) cudaEventRecord(plan->ev[0], st);
-  S2_CUDA(s2::launch_compress(plan->p, g, bitmap, table, cnt, S2_MASK_NONZERO, st, counters == nullptr),
+  S2_CUDA(s2::launch_compress(plan->p, g, bitmap, table, cnt, S2_MASK_NONZERO, st, counters == nullptr,
+                              split_list(plan)),
           "s2_reduce/compress");
   if (plan->ev[1]) cudaEventRecord(plan->ev[1], st);
   const uint32_t* un = bitmap;

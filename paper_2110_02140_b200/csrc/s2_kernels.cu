@@ -586,6 +586,88 @@ k_compress_tma(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* _
   }
 }
 
+// ---------------------------------------- compress, split variant: K1 (scan) + K2 (insert)
+//
+// K1 k_scan_compact: one warp per 1024-element tile (non-persistent grid, so the block
+// scheduler balances the tail): coalesced float4 loads, non-zero word by shuffle
+// transpose, bitmap store, then the tile's non-zeros are compacted (warp scan + one
+// atomicAdd per tile for the list offset) into a global (index, value) list.  No hashing
+// here, so the kernel is a lean streaming pass.
+// K2 k_insert_list: every thread takes list entries and does the r hashes + r
+// red.global.add.f32 — all 32 lanes busy, no per-warp queue.
+__global__ void __launch_bounds__(kThreads)
+k_scan_compact(const float* __restrict__ g, int64_t dim, uint32_t* __restrict__ bitmap, uint2* __restrict__ list,
+               unsigned long long* __restrict__ counters) {
+  __shared__ __align__(16) float4 s_tile[kWarps][kTile / 4];
+  griddep_wait();
+  griddep_launch_dependents();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t t = (int64_t)blockIdx.x * kWarps + wib;
+  const int64_t ntiles = (dim + kTile - 1) / kTile;
+  if (t >= ntiles) return;
+  const int64_t base = t * kTile;
+  const int64_t nelem_words = (dim + 31) / 32;
+  float4 v[8];
+  load_tile(v, g, t, dim, lane);
+  uint32_t m = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    m |= ((uint32_t)(v[k].x != 0.f) << (4 * k)) | ((uint32_t)(v[k].y != 0.f) << (4 * k + 1)) |
+         ((uint32_t)(v[k].z != 0.f) << (4 * k + 2)) | ((uint32_t)(v[k].w != 0.f) << (4 * k + 3));
+  }
+  const int cnt = __popc(m);
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int n = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += n;
+  }
+  const int total = __shfl_sync(kFull, incl, 31);
+  uint32_t word = 0;
+  if (total) {
+    const int src_grp = 8 * (lane & 3), src_sh = 4 * (lane >> 2);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint32_t mq = __shfl_sync(kFull, m, src_grp + q);
+      word |= ((mq >> src_sh) & 0xFu) << (4 * q);
+    }
+    unsigned long long off = 0;
+    if (lane == 0) off = atomicAdd(counters + S2_CNT_NNZ, (unsigned long long)total);
+    off = __shfl_sync(kFull, off, 0);
+    float4* st = s_tile[wib];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) st[k * 32 + lane] = v[k];
+    __syncwarp();
+    const float* sf = reinterpret_cast<const float*>(st);
+    unsigned long long pos = off + (unsigned long long)(incl - cnt);
+    for (uint32_t mm = m; mm; mm &= mm - 1u) {
+      const int b = __ffs(mm) - 1;
+      const uint32_t o = 128u * (uint32_t)(b >> 2) + 4u * lane + (uint32_t)(b & 3);
+      list[pos++] = make_uint2((uint32_t)base + o, __float_as_uint(sf[o]));
+    }
+  }
+  if (t * 32 + lane < nelem_words) bitmap[t * 32 + lane] = word;
+}
+
+template <int R>
+__global__ void __launch_bounds__(256)
+k_insert_list(const uint2* __restrict__ list, float* __restrict__ table, unsigned long long* __restrict__ counters,
+              const __grid_constant__ HashParams hp) {
+  griddep_wait();  // the list and its length come from k_scan_compact
+  griddep_launch_dependents();
+  const unsigned long long n = counters[S2_CNT_NNZ];
+  uint32_t bad = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)n; i += stride) {
+    const uint2 e = __ldcs(list + i);
+    const float v = __uint_as_float(e.y);
+    bad |= nonfinite(v);
+    insert_one<R>(e.x, v, table, hp);
+  }
+  if (__any_sync(kFull, bad) && (threadIdx.x & 31) == 0) atomicOr(counters + S2_CNT_NONFINITE, 1ull);
+  if (blockIdx.x == 0 && threadIdx.x == 0) counters[S2_CNT_SELECTED] = n;
+}
+
 // ---------------------------------------------------------------- decode (K4)
 
 // zt/zc: the NEXT reduce's sketch table and counters, zeroed here so that the next
@@ -897,7 +979,7 @@ static void launch_compress_r(const Plan& p, const float* g, uint32_t* bitmap, f
 }
 
 cudaError_t launch_compress(const Plan& p, const float* g, uint32_t* bitmap, float* table,
-                            unsigned long long* counters, int mode, cudaStream_t st, bool prezeroed) {
+                            unsigned long long* counters, int mode, cudaStream_t st, bool prezeroed, void* list) {
   cudaError_t e = cudaSuccess;
   if (!prezeroed) {
     e = cudaMemsetAsync(table, 0, sizeof(float) * (size_t)p.hp.rows * p.hp.cols, st);
@@ -908,6 +990,22 @@ cudaError_t launch_compress(const Plan& p, const float* g, uint32_t* bitmap, flo
   if (mode == S2_MASK_NONZERO && p.block_size > 1) {
     e = cudaMemsetAsync(bitmap, 0, sizeof(uint32_t) * (size_t)p.words, st);
     if (e != cudaSuccess) return e;
+  }
+  if (list != nullptr && mode == S2_MASK_NONZERO && p.block_size == 1) {
+    const int64_t ntiles = (p.dim + kTile - 1) / kTile;
+    e = launch_ex(k_scan_compact, (int)((ntiles + kWarps - 1) / kWarps), kThreads, 0, st, g, p.dim, bitmap,
+                  reinterpret_cast<uint2*>(list), counters);
+    if (e != cudaSuccess) return e;
+    const int grid = num_sms() * 8;
+    switch (p.hp.rows) {
+#define S2_CASE(r) \
+  case r: e = launch_ex(k_insert_list<r>, grid, 256, 0, st, reinterpret_cast<const uint2*>(list), table, counters, p.hp); break;
+      S2_CASE(1) S2_CASE(2) S2_CASE(3) S2_CASE(4) S2_CASE(5) S2_CASE(6) S2_CASE(7) S2_CASE(8)
+#undef S2_CASE
+      default: e = launch_ex(k_insert_list<0>, grid, 256, 0, st, reinterpret_cast<const uint2*>(list), table, counters, p.hp);
+    }
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
   }
   switch (p.hp.rows) {
     case 1: launch_compress_r<1>(p, g, bitmap, table, counters, mode, st); break;

@@ -20,7 +20,8 @@ struct Plan {
 };
 
 cudaError_t launch_compress(const Plan& p, const float* g, uint32_t* bitmap, float* table,
-                            unsigned long long* counters, int mode, cudaStream_t st, bool prezeroed = false);
+                            unsigned long long* counters, int mode, cudaStream_t st, bool prezeroed = false,
+                            void* list = nullptr);  // list: dim x 8 B scratch -> split K1 + K2 path
 constexpr int kMaxWorld = 8;
 // bitmaps of every rank (peer-mapped) whose OR the decode reads directly; n = 0: use `bitmap`
 struct PeerMaps {
