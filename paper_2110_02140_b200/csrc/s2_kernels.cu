@@ -599,21 +599,24 @@ __global__ void __launch_bounds__(kThreads)
 k_scan_compact(const float* __restrict__ g, int64_t dim, uint32_t* __restrict__ bitmap, uint2* __restrict__ list,
                unsigned long long* __restrict__ counters) {
   __shared__ __align__(16) float4 s_tile[kWarps][kTile / 4];
+  __shared__ int s_tot[kWarps];
+  __shared__ unsigned long long s_base;
   griddep_wait();
   griddep_launch_dependents();
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t t = (int64_t)blockIdx.x * kWarps + wib;
   const int64_t ntiles = (dim + kTile - 1) / kTile;
-  if (t >= ntiles) return;
   const int64_t base = t * kTile;
   const int64_t nelem_words = (dim + 31) / 32;
   float4 v[8];
-  load_tile(v, g, t, dim, lane);
   uint32_t m = 0;
+  if (t < ntiles) {
+    load_tile(v, g, t, dim, lane);
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    m |= ((uint32_t)(v[k].x != 0.f) << (4 * k)) | ((uint32_t)(v[k].y != 0.f) << (4 * k + 1)) |
-         ((uint32_t)(v[k].z != 0.f) << (4 * k + 2)) | ((uint32_t)(v[k].w != 0.f) << (4 * k + 3));
+    for (int k = 0; k < 8; ++k) {
+      m |= ((uint32_t)(v[k].x != 0.f) << (4 * k)) | ((uint32_t)(v[k].y != 0.f) << (4 * k + 1)) |
+           ((uint32_t)(v[k].z != 0.f) << (4 * k + 2)) | ((uint32_t)(v[k].w != 0.f) << (4 * k + 3));
+    }
   }
   const int cnt = __popc(m);
   int incl = cnt;
@@ -623,6 +626,20 @@ k_scan_compact(const float* __restrict__ g, int64_t dim, uint32_t* __restrict__ 
     if (lane >= o) incl += n;
   }
   const int total = __shfl_sync(kFull, incl, 31);
+  if (lane == 0) s_tot[wib] = total;
+  __syncthreads();
+  // one list reservation per CTA (not per tile): the counter sees gridDim.x atomics
+  if (threadIdx.x == 0) {
+    int sum = 0;
+    for (int w = 0; w < kWarps; ++w) {
+      const int c = s_tot[w];
+      s_tot[w] = sum;
+      sum += c;
+    }
+    s_base = sum ? atomicAdd(counters + S2_CNT_NNZ, (unsigned long long)sum) : 0ull;
+  }
+  __syncthreads();
+  if (t >= ntiles) return;
   uint32_t word = 0;
   if (total) {
     const int src_grp = 8 * (lane & 3), src_sh = 4 * (lane >> 2);
@@ -631,15 +648,12 @@ k_scan_compact(const float* __restrict__ g, int64_t dim, uint32_t* __restrict__ 
       const uint32_t mq = __shfl_sync(kFull, m, src_grp + q);
       word |= ((mq >> src_sh) & 0xFu) << (4 * q);
     }
-    unsigned long long off = 0;
-    if (lane == 0) off = atomicAdd(counters + S2_CNT_NNZ, (unsigned long long)total);
-    off = __shfl_sync(kFull, off, 0);
     float4* st = s_tile[wib];
 #pragma unroll
     for (int k = 0; k < 8; ++k) st[k * 32 + lane] = v[k];
     __syncwarp();
     const float* sf = reinterpret_cast<const float*>(st);
-    unsigned long long pos = off + (unsigned long long)(incl - cnt);
+    unsigned long long pos = s_base + (unsigned long long)(s_tot[wib] + incl - cnt);
     for (uint32_t mm = m; mm; mm &= mm - 1u) {
       const int b = __ffs(mm) - 1;
       const uint32_t o = 128u * (uint32_t)(b >> 2) + 4u * lane + (uint32_t)(b & 3);
