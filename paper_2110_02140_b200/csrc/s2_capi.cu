@@ -216,7 +216,7 @@ static void* split_list(const s2_plan* cplan) {
   s2_plan* plan = const_cast<s2_plan*>(cplan);  // lazily allocated scratch, not observable state
   if (plan->split < 0) {
     const char* e = getenv("S2_COMPRESS_SPLIT");
-    plan->split = e ? atoi(e) : 1;
+    plan->split = e ? atoi(e) : 0;  // opt-in: measured slower than the fused kernel
   }
   if (!plan->split || plan->p.block_size != 1) return nullptr;
   if (!plan->list && cudaMalloc(&plan->list, sizeof(uint64_t) * (size_t)plan->p.dim) != cudaSuccess) {
