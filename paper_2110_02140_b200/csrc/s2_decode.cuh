@@ -105,7 +105,6 @@ __device__ __forceinline__ void zero_next(float4* __restrict__ zt, int64_t zt_n4
 // Decode one warp tile (1024 elements at `base`) given its 32 union words (one per lane):
 // set positions are compacted by a warp scan into q, values (r gathers + lower median +
 // IEEE /W) land in vals, and the tile is written as dense float4 streaming stores.
-// Precondition: vals[0..1023] == 0 on entry (decode_zero_vals once per warp); restored on exit.
 template <int R>
 __device__ __forceinline__ void decode_tile(const DecodeCtx& c, int64_t base, uint32_t word, const HashParams& hp,
                                             uint16_t* q, float* vals) {
@@ -130,34 +129,28 @@ __device__ __forceinline__ void decode_tile(const DecodeCtx& c, int64_t base, ui
   }
   __syncwarp();
   const bool full = base + kDecTile <= dim;
-  if (full) {
-    // vals is all zeros except this tile's set positions (invariant kept by the reset below),
-    // so the dense tile is a straight copy: 8 x (LDS.128 + STG.128) per lane, no per-chunk masks
-    const float4* v4 = reinterpret_cast<const float4*>(vals);
-    float4* o4 = reinterpret_cast<float4*>(c.out + base);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) __stcs(o4 + k * 32 + lane, v4[k * 32 + lane]);
-  } else {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const float4 sv = reinterpret_cast<const float4*>(vals)[k * 32 + lane];
-      const int64_t e = base + k * 128 + lane * 4;
-      if (e + 0 < dim) c.out[e + 0] = sv.x;
-      if (e + 1 < dim) c.out[e + 1] = sv.y;
-      if (e + 2 < dim) c.out[e + 2] = sv.z;
-      if (e + 3 < dim) c.out[e + 3] = sv.w;
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t wk = __shfl_sync(kFull, word, 4 * k + (lane >> 3));
+    const uint32_t nib = (wk >> ((lane & 7) * 4)) & 0xFu;
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (nib) {
+      const float4 sv = *reinterpret_cast<const float4*>(vals + k * 128 + lane * 4);
+      o.x = (nib & 1u) ? sv.x : 0.f;
+      o.y = (nib & 2u) ? sv.y : 0.f;
+      o.z = (nib & 4u) ? sv.z : 0.f;
+      o.w = (nib & 8u) ? sv.w : 0.f;
+    }
+    const int64_t e = base + k * 128 + lane * 4;
+    if (full) {
+      __stcs(reinterpret_cast<float4*>(c.out + e), o);
+    } else {
+      if (e + 0 < dim) c.out[e + 0] = o.x;
+      if (e + 1 < dim) c.out[e + 1] = o.y;
+      if (e + 2 < dim) c.out[e + 2] = o.z;
+      if (e + 3 < dim) c.out[e + 3] = o.w;
     }
   }
-  __syncwarp();
-  for (int s = lane; s < total; s += 32) vals[q[s]] = 0.f;  // restore the all-zero invariant
-  __syncwarp();
-}
-
-__device__ __forceinline__ void decode_zero_vals(float* vals) {
-  const int lane = threadIdx.x & 31;
-  float4* v4 = reinterpret_cast<float4*>(vals);
-#pragma unroll
-  for (int k = 0; k < 8; ++k) v4[k * 32 + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
   __syncwarp();
 }
 
@@ -168,7 +161,6 @@ __device__ __forceinline__ void decode_range(const DecodeCtx& c, const PeerMaps&
                                              int64_t tend, const HashParams& hp, uint16_t* q, float* vals) {
   const int lane = threadIdx.x & 31;
   const int64_t nelem_words = (c.dim + 31) / 32;
-  decode_zero_vals(vals);
   int64_t t = t0;
   uint32_t wnext = t < tend ? decode_word<BLOCKS>(c.bitmap, pm, t, lane, c.dim, c.bs, nelem_words) : 0u;
   for (; t < tend; t += tstep) {
@@ -199,7 +191,6 @@ __device__ __forceinline__ void decode_range_peers(const DecodeCtx& c, const Pee
     if (e0 + 32 > c.dim) w &= e0 >= c.dim ? 0u : range_mask(0, (int)(c.dim - e0));
     return w;
   };
-  decode_zero_vals(vals);
   uint32_t cur[kAhead];
 #pragma unroll
   for (int k = 0; k < kAhead; ++k) cur[k] = fetch(t0 + (int64_t)k * tstep);

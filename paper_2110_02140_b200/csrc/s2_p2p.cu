@@ -550,17 +550,13 @@ k_xdecode(const __grid_constant__ P2PArgs a, const __grid_constant__ DecodeCtx d
   c.bitmap = un;
   c.table = ONESHOT ? reinterpret_cast<const float*>(a.base[me] + a.off_tsum[cur])
                     : reinterpret_cast<const float*>(a.base[me] + a.off_table[cur]);
-  (void)none;
-  decode_zero_vals(s_v[wib]);
-  const int64_t nelem_words = (dc.dim + 31) / 32;
   for (;;) {
     int k = 0;
     if (lane == 0) k = atomicAdd(&s_next, 1);
     k = __shfl_sync(kFull, k, 0);
     const int64_t t = tb + k;
     if (t >= te) break;
-    decode_tile<R>(c, t * kDecTile, decode_word<false>(c.bitmap, none, t, lane, dc.dim, 1, nelem_words), hp,
-                   s_q[wib], s_v[wib]);
+    decode_range<R, false>(c, none, t, 1, t + 1, hp, s_q[wib], s_v[wib]);
   }
   S2_TRACE(4);
 }
