@@ -378,6 +378,8 @@ static int64_t layout_p2p(s2_plan* plan, int W, int G) {
   a.rank = plan->rank;
   a.mc = nullptr;
   a.nvls = 0;
+  const char* hv = getenv("S2_P2P_HIER");
+  a.hier = hv ? atoi(hv) : 0;
   return off;
 }
 

@@ -64,6 +64,7 @@ struct P2PArgs {
   int table_only;             // 1: bitmaps are OR-ed by the decode from peer memory (no bitmap exchange)
   char* mc;                   // NVLS multicast address of the arena (nullptr: none)
   int nvls;                   // 1: reduce in the NVSwitch (multimem.ld_reduce / multimem.st)
+  int hier;                   // 1: hierarchical barriers (CTA 0 <-> peers, local release)
   unsigned long long* trace;  // optional: per-CTA globaltimer stamps [G][8] (S2_P2P_TRACE=1)
 };
 cudaError_t launch_p2p_aggregate(const P2PArgs& a, int grid, cudaStream_t st);

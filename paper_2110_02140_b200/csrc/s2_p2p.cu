@@ -81,6 +81,75 @@ __device__ __forceinline__ uint64_t globaltimer() {
       a.trace[(int64_t)blockIdx.x * 8 + (slot)] = globaltimer();                \
   } while (0)
 
+struct XSync {
+  unsigned long long* arrive;  // local arrival counter (cumulative)
+  uint32_t* release;           // CTA 0 -> local CTAs: last cross-rank epoch passed (x2 per call)
+};
+
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_gpu64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// all CTAs of this grid arrive; returns when `target` arrivals were counted
+__device__ __forceinline__ void local_arrive_wait(unsigned long long* arrive, unsigned long long target,
+                                                  bool wait_all) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(arrive, 1ull);
+    if (wait_all)
+      while (ld_acquire_gpu64(arrive) < target) {
+      }
+  }
+  __syncthreads();
+}
+
+// CTA 0 <-> CTA 0 of every rank (flag slot [rank] of each rank's array), then release locally
+template <int W>
+__device__ __forceinline__ void rank_barrier(const P2PArgs& a, int64_t off_flags, uint32_t ep, uint32_t* release,
+                                             uint32_t rel_val) {
+  if (blockIdx.x == 0) {
+    if (threadIdx.x < W) {
+      const int q = threadIdx.x;
+      st_release_sys(reinterpret_cast<uint32_t*>(a.base[q] + off_flags) + a.rank, ep);
+      const uint32_t* mine = reinterpret_cast<const uint32_t*>(a.base[a.rank] + off_flags) + q;
+      uint64_t t0 = 0;
+      for (int spin = 0; (int32_t)(ld_acquire_sys(mine) - ep) < 0; ++spin) {
+        if ((spin & 1023) == 1023) {
+          const uint64_t now = globaltimer();
+          if (t0 == 0) t0 = now;
+          else if (now - t0 > 10000000000ull) {
+            atomicOr(reinterpret_cast<uint32_t*>(a.base[a.rank] + a.off_error), 1u);
+            break;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) st_release_gpu(release, rel_val);
+  } else if (threadIdx.x == 0) {
+    uint64_t t0 = 0;
+    for (int spin = 0; (int32_t)(ld_acquire_gpu(release) - rel_val) < 0; ++spin) {
+      if ((spin & 1023) == 1023) {
+        const uint64_t now = globaltimer();
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > 10000000000ull) break;
+      }
+    }
+  }
+  __syncthreads();
+}
+
 constexpr int kP2PThreads = 1024;
 // vectors per thread whose W loads are all in flight together (register budget: 64/thread)
 template <int W>
@@ -181,7 +250,10 @@ __global__ void __launch_bounds__(kP2PThreads) k_p2p_aggregate(const __grid_cons
   const int64_t w4 = a.table_only ? 0 : a.words / 4 / W;  // ... and bitmap (unless the decode ORs them)
   int64_t lo, hi;
   chunk_of(t4 + w4, lo, hi);
-  cross_rank_barrier<W>(a, a.off_flags_a, ep);
+  unsigned long long* arrive = reinterpret_cast<unsigned long long*>(a.base[a.rank] + a.off_lsync);
+  uint32_t* release = reinterpret_cast<uint32_t*>(a.base[a.rank] + a.off_lsync + 8);
+  if (a.hier) rank_barrier<W>(a, a.off_flags_a, ep, release, 2u * ep - 1u);
+  else cross_rank_barrier<W>(a, a.off_flags_a, ep);
   S2_TRACE(1);
   // peers are all in this reduce now: the decode may launch (its prologue zeroes the NEXT
   // ping-pong table, which no peer reads any more)
@@ -189,7 +261,12 @@ __global__ void __launch_bounds__(kP2PThreads) k_p2p_aggregate(const __grid_cons
   for (int64_t i0 = lo + threadIdx.x; i0 < hi; i0 += (int64_t)p2p_batch<W>() * kP2PThreads)
     reduce_batch<W>(a, i0, hi, t4, w4);  // phase A: reduce-scatter
   S2_TRACE(2);
-  cross_rank_barrier<W>(a, a.off_flags_b, ep);
+  if (a.hier) {  // all local CTAs' slices written -> CTA 0 <-> peers -> local release
+    local_arrive_wait(arrive, (unsigned long long)ep * gridDim.x, blockIdx.x == 0);
+    rank_barrier<W>(a, a.off_flags_b, ep, release, 2u * ep);
+  } else {
+    cross_rank_barrier<W>(a, a.off_flags_b, ep);
+  }
   S2_TRACE(3);
   for (int64_t i0 = lo + threadIdx.x; i0 < hi; i0 += (int64_t)p2p_batch<W>() * kP2PThreads)
     gather_batch<W>(a, i0, hi, t4, w4);  // phase B: all-gather
@@ -215,7 +292,9 @@ __global__ void __launch_bounds__(kP2PThreads) k_p2p_oneshot(const __grid_consta
   const int64_t t4 = a.cells / 4, w4 = a.table_only ? 0 : a.words / 4;
   int64_t lo, hi;
   chunk_of(t4 + w4, lo, hi);
-  cross_rank_barrier<W>(a, a.off_flags_a, s_ep);
+  if (a.hier) rank_barrier<W>(a, a.off_flags_a, s_ep, reinterpret_cast<uint32_t*>(a.base[a.rank] + a.off_lsync + 8),
+                              2u * s_ep - 1u);
+  else cross_rank_barrier<W>(a, a.off_flags_a, s_ep);
   S2_TRACE(1);
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   constexpr int B = p2p_batch<W>();
@@ -354,75 +433,6 @@ __global__ void __launch_bounds__(kP2PThreads) k_nvls_exchange(const __grid_cons
 // bitmaps, peer loads batched with the table loads), so only the table needs the grid
 // barrier.  Table: one-shot (W <= 2 by default) or two-shot (reduce-scatter, barrier,
 // all-gather).
-struct XSync {
-  unsigned long long* arrive;  // local arrival counter (cumulative)
-  uint32_t* release;           // CTA 0 -> local CTAs: last cross-rank epoch passed (x2 per call)
-};
-
-__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ unsigned long long ld_acquire_gpu64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-// all CTAs of this grid arrive; returns when `target` arrivals were counted
-__device__ __forceinline__ void local_arrive_wait(unsigned long long* arrive, unsigned long long target,
-                                                  bool wait_all) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(arrive, 1ull);
-    if (wait_all)
-      while (ld_acquire_gpu64(arrive) < target) {
-      }
-  }
-  __syncthreads();
-}
-
-// CTA 0 <-> CTA 0 of every rank (flag slot [rank] of each rank's array), then release locally
-template <int W>
-__device__ __forceinline__ void rank_barrier(const P2PArgs& a, int64_t off_flags, uint32_t ep, uint32_t* release,
-                                             uint32_t rel_val) {
-  if (blockIdx.x == 0) {
-    if (threadIdx.x < W) {
-      const int q = threadIdx.x;
-      st_release_sys(reinterpret_cast<uint32_t*>(a.base[q] + off_flags) + a.rank, ep);
-      const uint32_t* mine = reinterpret_cast<const uint32_t*>(a.base[a.rank] + off_flags) + q;
-      uint64_t t0 = 0;
-      for (int spin = 0; (int32_t)(ld_acquire_sys(mine) - ep) < 0; ++spin) {
-        if ((spin & 1023) == 1023) {
-          const uint64_t now = globaltimer();
-          if (t0 == 0) t0 = now;
-          else if (now - t0 > 10000000000ull) {
-            atomicOr(reinterpret_cast<uint32_t*>(a.base[a.rank] + a.off_error), 1u);
-            break;
-          }
-        }
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) st_release_gpu(release, rel_val);
-  } else if (threadIdx.x == 0) {
-    uint64_t t0 = 0;
-    for (int spin = 0; (int32_t)(ld_acquire_gpu(release) - rel_val) < 0; ++spin) {
-      if ((spin & 1023) == 1023) {
-        const uint64_t now = globaltimer();
-        if (t0 == 0) t0 = now;
-        else if (now - t0 > 10000000000ull) break;
-      }
-    }
-  }
-  __syncthreads();
-}
-
 template <int R, int W, bool ONESHOT>
 __global__ void __launch_bounds__(256, 4)
 k_xdecode(const __grid_constant__ P2PArgs a, const __grid_constant__ DecodeCtx dc, const __grid_constant__ HashParams hp,

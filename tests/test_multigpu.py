@@ -25,6 +25,7 @@ VARIANTS = {
     "fused": {"S2_FUSED": "1"},                # exchange + decode in one kernel
     "bitmap_in_decode": {"S2_P2P_BITMAP_IN_DECODE_MAXW": "8"},  # decode ORs peer bitmaps over NVLink
     "graph": {"S2_CHECK_GRAPH": "1"},          # CUDA-graph replay of the whole reduce
+    "hier": {"S2_P2P_HIER": "1"},              # hierarchical cross-rank barriers
 }
 
 
