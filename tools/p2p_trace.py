@@ -27,7 +27,8 @@ g = torch.from_numpy(o.synthetic_gradient(d, 0.01, rank)).cuda()
 out = torch.empty(d, device="cuda")
 res = []
 for it in range(30):
-    red.reduce(g, out=out)
+    for _ in range(8):  # back-to-back (no host sync between reduces): steady-state skew
+        red.reduce(g, out=out)
     torch.cuda.synchronize()
     if it >= 10:
         G = torch.cuda.get_device_properties(0).multi_processor_count * 8
