@@ -358,8 +358,8 @@ static int64_t layout_p2p(s2_plan* plan, int W, int G) {
   for (int k = 0; k < 2; ++k) a.off_table[k] = take(cells * 4);
   for (int k = 0; k < 2; ++k) a.off_bitmap[k] = take(words * 4);
   for (int k = 0; k < 2; ++k) a.off_union[k] = take(words * 4);
-  a.off_flags_a = take((int64_t)W * G * 4);
-  a.off_flags_b = take((int64_t)W * G * 4);
+  a.off_flags_a = take((int64_t)W * 8 * G * 4);  // exchange grids up to 8 CTAs/SM (S2_P2P_GRID)
+  a.off_flags_b = take((int64_t)W * 8 * G * 4);
   a.off_epoch = take((int64_t)8 * G * 4);  // per-CTA epochs (fused grid <= 8 CTAs/SM)
   a.off_error = take(256);
   a.off_lsync = take(256);
@@ -395,6 +395,8 @@ static int finish_p2p(s2_plan* plan, int G) {
   s2::P2PArgs& a = plan->pa;
   const int W = plan->world;
   plan->p2p_grid = G;
+  const char* ge = getenv("S2_P2P_GRID");  // exchange-kernel CTAs (default: one per SM)
+  if (ge && atoi(ge) > 0 && atoi(ge) <= 8 * G) plan->p2p_grid = atoi(ge);
   plan->p2p = true;
   a.trace = nullptr;
   const char* tr = getenv("S2_P2P_TRACE");
