@@ -363,6 +363,9 @@ static int64_t layout_p2p(s2_plan* plan, int W, int G) {
   a.off_epoch = take((int64_t)8 * G * 4);  // per-CTA epochs (fused grid <= 8 CTAs/SM)
   a.off_error = take(256);
   a.off_lsync = take(256);
+  a.off_flags_c = take(256);  // [rank] = that rank's last compress epoch (signal_done)
+  a.off_cdone = take(256);    // this rank's compress CTA-done counter
+  a.off_cepoch = take(256);   // this rank's compress epoch
   const char* os_env = getenv("S2_P2P_ONESHOT_MAXW");
   const int oneshot_maxw = os_env ? atoi(os_env) : 2;
   a.oneshot = (W <= oneshot_maxw && W <= 4) ? 1 : 0;
@@ -380,6 +383,8 @@ static int64_t layout_p2p(s2_plan* plan, int W, int G) {
   a.nvls = 0;
   const char* hv = getenv("S2_P2P_HIER");
   a.hier = hv ? atoi(hv) : 0;
+  const char* cs = getenv("S2_P2P_COMPRESS_SIGNAL");
+  a.csig = cs ? atoi(cs) : 0;
   return off;
 }
 
@@ -602,8 +607,18 @@ int s2_reduce(s2_plan* plan, const float* g, float* out, uint64_t* counters, voi
   // caller counters: zeroed by memset; plan counters: zeroed by the previous decode
   unsigned long long* cnt = counters ? reinterpret_cast<unsigned long long*>(counters) : plan->counters[cur];
   if (plan->ev[0]) cudaEventRecord(plan->ev[0], st);
+  s2::DoneSignal sig{};
+  const bool use_sig = plan->world > 1 && plan->p2p && plan->pa.csig && !plan->pa.nvls && !plan->fused;
+  if (use_sig) {
+    sig.done = reinterpret_cast<unsigned int*>(plan->arena + plan->pa.off_cdone);
+    sig.epoch = reinterpret_cast<unsigned int*>(plan->arena + plan->pa.off_cepoch);
+    for (int q = 0; q < plan->world; ++q)
+      sig.peer_flags[q] = reinterpret_cast<uint32_t*>(plan->pa.base[q] + plan->pa.off_flags_c);
+    sig.world = plan->world;
+    sig.rank = plan->rank;
+  }
   S2_CUDA(s2::launch_compress(plan->p, g, bitmap, table, cnt, S2_MASK_NONZERO, st, counters == nullptr,
-                              split_list(plan)),
+                              use_sig ? nullptr : split_list(plan), use_sig ? &sig : nullptr),
           "s2_reduce/compress");
   if (plan->ev[1]) cudaEventRecord(plan->ev[1], st);
   const uint32_t* un = bitmap;

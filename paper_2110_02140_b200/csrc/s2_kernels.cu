@@ -152,6 +152,28 @@ __device__ __forceinline__ void load_tile(float4 (&v)[8], const float* __restric
   }
 }
 
+// ---- "this rank's compress is complete" signal (W > 1, peer-memory exchange) -------------
+// The last CTA to finish (threadFenceReduction pattern) bumps the compress epoch and stores
+// it with release semantics at system scope into slot [rank] of every rank's flag array, so
+// the exchange kernel's first barrier is a local poll instead of a round of NVLink flag
+// traffic issued only once its own CTAs have launched.
+__device__ __forceinline__ void signal_done(const DoneSignal& sig) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(sig.done, 1u);
+    if (prev == gridDim.x - 1) {
+      __threadfence();
+      const unsigned ep = *sig.epoch + 1u;
+      *sig.epoch = ep;
+      *sig.done = 0u;
+      __threadfence_system();
+      for (int q = 0; q < sig.world; ++q)
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(sig.peer_flags[q] + sig.rank), "r"(ep) : "memory");
+    }
+  }
+}
+
 // ---- TMA (cp.async.bulk) + mbarrier helpers -------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -203,7 +225,7 @@ template <int R, int MODE, int LOAD>
 __global__ void __launch_bounds__(kThreads, LOAD == 0 ? 2 : 4)
 k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __restrict__ bitmap,
            float* __restrict__ table, unsigned long long* __restrict__ counters,
-           const __grid_constant__ HashParams hp) {
+           const __grid_constant__ HashParams hp, const __grid_constant__ DoneSignal sig) {
   constexpr int kCap = 32 + kQFast;
   __shared__ uint32_t s_qi[kWarps][kCap];
   __shared__ float s_qv[kWarps][kCap];
@@ -406,6 +428,7 @@ k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __res
     if (MODE == 2 && sel) atomicAdd(counters + S2_CNT_SELECTED, sel);
     if (bad) atomicOr(counters + S2_CNT_NONFINITE, 1ull);
   }
+  if (sig.done != nullptr) signal_done(sig);
 }
 
 // ------------------------------------------- compress, TMA-staged variant (default)
@@ -942,7 +965,7 @@ static int compress_variant() {
 
 template <int R, int LOAD>
 static void launch_compress_rm(const Plan& p, const float* g, uint32_t* bitmap, float* table,
-                               unsigned long long* counters, int mode, cudaStream_t st) {
+                               unsigned long long* counters, int mode, cudaStream_t st, const DoneSignal& sig) {
   const int64_t ntiles = (p.dim + kTile - 1) / kTile;
   static int waves = -1;  // S2_COMPRESS_CTAS_PER_SM: grid = SMs x this (>= resident -> extra waves)
   if (waves < 0) {
@@ -951,11 +974,14 @@ static void launch_compress_rm(const Plan& p, const float* g, uint32_t* bitmap, 
   }
   const int grid = grid_for(ntiles, waves > 0 ? waves : (LOAD == 0 ? 2 : 4));
   if (mode == S2_MASK_GIVEN) {
-    launch_ex(k_compress<R, 2, LOAD>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table, counters, p.hp);
+    launch_ex(k_compress<R, 2, LOAD>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table, counters, p.hp,
+              sig);
   } else if (p.block_size == 1) {
-    launch_ex(k_compress<R, 0, LOAD>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table, counters, p.hp);
+    launch_ex(k_compress<R, 0, LOAD>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table, counters, p.hp,
+              sig);
   } else {
-    launch_ex(k_compress<R, 1, LOAD>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table, counters, p.hp);
+    launch_ex(k_compress<R, 1, LOAD>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table, counters, p.hp,
+              sig);
   }
 }
 
@@ -977,14 +1003,14 @@ static void launch_compress_tma(const Plan& p, const float* g, uint32_t* bitmap,
 
 template <int R>
 static void launch_compress_r(const Plan& p, const float* g, uint32_t* bitmap, float* table,
-                              unsigned long long* counters, int mode, cudaStream_t st) {
-  const int v = compress_variant();
+                              unsigned long long* counters, int mode, cudaStream_t st, const DoneSignal& sig) {
+  const int v = sig.done != nullptr ? 0 : compress_variant();  // the done signal lives in k_compress
   if (v == 0) {
-    launch_compress_rm<R, 0>(p, g, bitmap, table, counters, mode, st);
+    launch_compress_rm<R, 0>(p, g, bitmap, table, counters, mode, st, sig);
   } else if (v == 3) {
-    launch_compress_rm<R, 3>(p, g, bitmap, table, counters, mode, st);
+    launch_compress_rm<R, 3>(p, g, bitmap, table, counters, mode, st, sig);
   } else if (v == 1) {
-    launch_compress_rm<R, 1>(p, g, bitmap, table, counters, mode, st);
+    launch_compress_rm<R, 1>(p, g, bitmap, table, counters, mode, st, sig);
   } else {
     if (mode == S2_MASK_GIVEN) launch_compress_tma<R, 2>(p, g, bitmap, table, counters, st);
     else if (p.block_size == 1) launch_compress_tma<R, 0>(p, g, bitmap, table, counters, st);
@@ -993,7 +1019,10 @@ static void launch_compress_r(const Plan& p, const float* g, uint32_t* bitmap, f
 }
 
 cudaError_t launch_compress(const Plan& p, const float* g, uint32_t* bitmap, float* table,
-                            unsigned long long* counters, int mode, cudaStream_t st, bool prezeroed, void* list) {
+                            unsigned long long* counters, int mode, cudaStream_t st, bool prezeroed, void* list,
+                            const DoneSignal* signal) {
+  DoneSignal sig{};
+  if (signal != nullptr) sig = *signal;
   cudaError_t e = cudaSuccess;
   if (!prezeroed) {
     e = cudaMemsetAsync(table, 0, sizeof(float) * (size_t)p.hp.rows * p.hp.cols, st);
@@ -1005,7 +1034,7 @@ cudaError_t launch_compress(const Plan& p, const float* g, uint32_t* bitmap, flo
     e = cudaMemsetAsync(bitmap, 0, sizeof(uint32_t) * (size_t)p.words, st);
     if (e != cudaSuccess) return e;
   }
-  if (list != nullptr && mode == S2_MASK_NONZERO && p.block_size == 1) {
+  if (list != nullptr && mode == S2_MASK_NONZERO && p.block_size == 1 && sig.done == nullptr) {
     const int64_t ntiles = (p.dim + kTile - 1) / kTile;
     e = launch_ex(k_scan_compact, (int)((ntiles + kWarps - 1) / kWarps), kThreads, 0, st, g, p.dim, bitmap,
                   reinterpret_cast<uint2*>(list), counters);
@@ -1022,10 +1051,10 @@ cudaError_t launch_compress(const Plan& p, const float* g, uint32_t* bitmap, flo
     return cudaGetLastError();
   }
   switch (p.hp.rows) {
-    case 1: launch_compress_r<1>(p, g, bitmap, table, counters, mode, st); break;
-    case 3: launch_compress_r<3>(p, g, bitmap, table, counters, mode, st); break;
-    case 5: launch_compress_r<5>(p, g, bitmap, table, counters, mode, st); break;
-    default: launch_compress_r<0>(p, g, bitmap, table, counters, mode, st); break;
+    case 1: launch_compress_r<1>(p, g, bitmap, table, counters, mode, st, sig); break;
+    case 3: launch_compress_r<3>(p, g, bitmap, table, counters, mode, st, sig); break;
+    case 5: launch_compress_r<5>(p, g, bitmap, table, counters, mode, st, sig); break;
+    default: launch_compress_r<0>(p, g, bitmap, table, counters, mode, st, sig); break;
   }
   if (mode == S2_MASK_NONZERO && p.block_size > 1) {
     e = cudaGetLastError();

@@ -19,9 +19,17 @@ struct Plan {
   HashParams hp;
 };
 
+constexpr int kMaxWorldSig = 8;
+struct DoneSignal {  // see signal_done (s2_kernels.cu); done == nullptr: no signal
+  unsigned int* done;
+  unsigned int* epoch;
+  uint32_t* peer_flags[kMaxWorldSig];
+  int world, rank;
+};
 cudaError_t launch_compress(const Plan& p, const float* g, uint32_t* bitmap, float* table,
                             unsigned long long* counters, int mode, cudaStream_t st, bool prezeroed = false,
-                            void* list = nullptr);  // list: dim x 8 B scratch -> split K1 + K2 path
+                            void* list = nullptr,  // list: dim x 8 B scratch -> split K1 + K2 path
+                            const DoneSignal* signal = nullptr);
 constexpr int kMaxWorld = 8;
 // bitmaps of every rank (peer-mapped) whose OR the decode reads directly; n = 0: use `bitmap`
 struct PeerMaps {
@@ -65,6 +73,8 @@ struct P2PArgs {
   char* mc;                   // NVLS multicast address of the arena (nullptr: none)
   int nvls;                   // 1: reduce in the NVSwitch (multimem.ld_reduce / multimem.st)
   int hier;                   // 1: hierarchical barriers (CTA 0 <-> peers, local release)
+  int csig;                   // 1: barrier 1 = poll of the compress-done flags (signal_done)
+  int64_t off_flags_c, off_cdone, off_cepoch;
   unsigned long long* trace;  // optional: per-CTA globaltimer stamps [G][8] (S2_P2P_TRACE=1)
 };
 cudaError_t launch_p2p_aggregate(const P2PArgs& a, int grid, cudaStream_t st);

@@ -61,6 +61,31 @@ __device__ __forceinline__ void cross_rank_barrier(const P2PArgs& a, int64_t off
   __syncthreads();
 }
 
+// Barrier 1 when the compress kernels signal completion themselves (a.csig): every rank's
+// last compress CTA stored its compress epoch into slot [rank] of this rank's flag array;
+// wait until all W slots reached the epoch our own compress wrote.
+template <int W>
+__device__ __forceinline__ void compress_done_barrier(const P2PArgs& a) {
+  if (threadIdx.x < W) {
+    const int q = threadIdx.x;
+    const uint32_t ep = *reinterpret_cast<volatile const uint32_t*>(a.base[a.rank] + a.off_cepoch);
+    const uint32_t* mine = reinterpret_cast<const uint32_t*>(a.base[a.rank] + a.off_flags_c) + q;
+    uint64_t t0 = 0;
+    for (int spin = 0; (int32_t)(ld_acquire_sys(mine) - ep) < 0; ++spin) {
+      if ((spin & 1023) == 1023) {
+        uint64_t now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > 10000000000ull) {
+          atomicOr(reinterpret_cast<uint32_t*>(a.base[a.rank] + a.off_error), 1u);
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
 // chunk [lo, hi) of n vectors for CTA b of G
 __device__ __forceinline__ void chunk_of(int64_t n, int64_t& lo, int64_t& hi) {
   const int64_t per = (n + gridDim.x - 1) / gridDim.x;
@@ -252,7 +277,8 @@ __global__ void __launch_bounds__(kP2PThreads) k_p2p_aggregate(const __grid_cons
   chunk_of(t4 + w4, lo, hi);
   unsigned long long* arrive = reinterpret_cast<unsigned long long*>(a.base[a.rank] + a.off_lsync);
   uint32_t* release = reinterpret_cast<uint32_t*>(a.base[a.rank] + a.off_lsync + 8);
-  if (a.hier) rank_barrier<W>(a, a.off_flags_a, ep, release, 2u * ep - 1u);
+  if (a.csig) compress_done_barrier<W>(a);
+  else if (a.hier) rank_barrier<W>(a, a.off_flags_a, ep, release, 2u * ep - 1u);
   else cross_rank_barrier<W>(a, a.off_flags_a, ep);
   S2_TRACE(1);
   // peers are all in this reduce now: the decode may launch (its prologue zeroes the NEXT
@@ -292,8 +318,9 @@ __global__ void __launch_bounds__(kP2PThreads) k_p2p_oneshot(const __grid_consta
   const int64_t t4 = a.cells / 4, w4 = a.table_only ? 0 : a.words / 4;
   int64_t lo, hi;
   chunk_of(t4 + w4, lo, hi);
-  if (a.hier) rank_barrier<W>(a, a.off_flags_a, s_ep, reinterpret_cast<uint32_t*>(a.base[a.rank] + a.off_lsync + 8),
-                              2u * s_ep - 1u);
+  if (a.csig) compress_done_barrier<W>(a);
+  else if (a.hier) rank_barrier<W>(a, a.off_flags_a, s_ep, reinterpret_cast<uint32_t*>(a.base[a.rank] + a.off_lsync + 8),
+                                   2u * s_ep - 1u);
   else cross_rank_barrier<W>(a, a.off_flags_a, s_ep);
   S2_TRACE(1);
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");

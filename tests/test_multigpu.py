@@ -26,6 +26,7 @@ VARIANTS = {
     "bitmap_in_decode": {"S2_P2P_BITMAP_IN_DECODE_MAXW": "8"},  # decode ORs peer bitmaps over NVLink
     "graph": {"S2_CHECK_GRAPH": "1"},          # CUDA-graph replay of the whole reduce
     "hier": {"S2_P2P_HIER": "1"},              # hierarchical cross-rank barriers
+    "csig": {"S2_P2P_COMPRESS_SIGNAL": "1"},   # compress kernels signal completion to the peers
 }
 
 
