@@ -14,8 +14,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libs2.so")
-SOURCES = ["s2_kernels.cu", "s2_p2p.cu", "s2_topk.cu", "s2_capi.cu"]
-HEADERS = ["s2_common.cuh", "s2_kernels.h", "s2_decode.cuh"]
+SOURCES = ["s2_compress.cu", "s2_decode.cu", "s2_kernels.cu", "s2_p2p.cu", "s2_topk.cu", "s2_capi.cu"]
+HEADERS = ["s2_common.cuh", "s2_kernels.h", "s2_decode.cuh", "s2_device.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -48,20 +48,37 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = True) -> str:
+    """Compile each .cu to an object in parallel (the kernels are template-heavy), then link."""
     if not force and not _stale():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
+
     inc, lib = nccl_dirs()
-    cmd = [
-        nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-        "-Xptxas", "-v" if verbose and os.environ.get("S2_PTXAS_V") else "-O3",
-        "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc,
-        *[os.path.join(CSRC, s) for s in SOURCES],
-        "-L", lib, "-l:libnccl.so.2", f"-Xlinker=-rpath={lib}",
-        "-o", LIB + ".tmp",
-    ]
+    objdir = os.path.join(PKG, "build_obj")
+    os.makedirs(objdir, exist_ok=True)
+    common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+              "-Xptxas", "-v" if verbose and os.environ.get("S2_PTXAS_V") else "-O3",
+              "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        cmd = common + ["-c", os.path.join(CSRC, src), "-o", obj]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.stdout or r.stderr:
+            sys.stderr.write(r.stdout + r.stderr)
+        if r.returncode:
+            raise subprocess.CalledProcessError(r.returncode, cmd)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
+    link = [nvcc(), *ARCH, "-shared", *objs, "-L", lib, "-l:libnccl.so.2", f"-Xlinker=-rpath={lib}",
+            "-o", LIB + ".tmp"]
     if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True)
+        print(" ".join(link), file=sys.stderr)
+    subprocess.run(link, check=True)
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -1,0 +1,67 @@
+// s2_decode.cu — the standalone K4 decode kernel and its launcher (body in s2_decode.cuh).
+#include "s2_device.cuh"
+#include "s2_decode.cuh"
+
+namespace s2 {
+
+// ---------------------------------------------------------------- decode (K4)
+
+// zt/zc: the NEXT reduce's sketch table and counters, zeroed here so that the next
+// compress needs no memset (plan ping-pong, s2_reduce); may be null.
+template <int R, bool BLOCKS>
+__global__ void __launch_bounds__(kThreads)
+k_decode(const uint32_t* __restrict__ bitmap, int64_t dim, int64_t bs,
+         const float* __restrict__ table, float workers, float inv_workers, int workers_pow2,
+         float* __restrict__ out, float4* __restrict__ zt, int64_t zt_n4,
+         unsigned long long* __restrict__ zc, const __grid_constant__ HashParams hp,
+         const __grid_constant__ PeerMaps pm) {
+  zero_next(zt, zt_n4, zc);
+  griddep_wait();  // bitmap + table come from the compress / exchange kernel
+  griddep_launch_dependents();
+  __shared__ uint16_t s_q[kWarps][kTile];
+  __shared__ __align__(16) float s_v[kWarps][kTile];
+  const int wib = threadIdx.x >> 5;
+  const int64_t ntiles = (dim + kTile - 1) / kTile;
+  DecodeCtx c{bitmap, table, out, dim, bs, workers, inv_workers, workers_pow2};
+  if (!BLOCKS && pm.n > 0)
+    decode_range_peers<R>(c, pm, (int64_t)blockIdx.x * kWarps + wib, (int64_t)gridDim.x * kWarps, ntiles, hp,
+                          s_q[wib], s_v[wib]);
+  else
+    decode_range<R, BLOCKS>(c, pm, (int64_t)blockIdx.x * kWarps + wib, (int64_t)gridDim.x * kWarps, ntiles, hp,
+                            s_q[wib], s_v[wib]);
+}
+
+template <int R>
+static void launch_decode_r(const Plan& p, const uint32_t* bitmap, const float* table, int workers,
+                            float* out, float* zt, unsigned long long* zc, const PeerMaps& pm, cudaStream_t st) {
+  const int64_t ntiles = (p.dim + kTile - 1) / kTile;
+  const int grid = grid_for(ntiles, 4);
+  const int pow2 = (workers & (workers - 1)) == 0;
+  const float inv = 1.0f / (float)workers;
+  const int64_t zn4 = zt ? ((int64_t)p.hp.rows * p.hp.cols + 3) / 4 : 0;
+  float4* z4 = reinterpret_cast<float4*>(zt);
+  if (p.block_size == 1)
+    launch_ex(k_decode<R, false>, grid, kThreads, 0, st, bitmap, p.dim, (int64_t)1, table, (float)workers, inv, pow2,
+              out, z4, zn4, zc, p.hp, pm);
+  else
+    launch_ex(k_decode<R, true>, grid, kThreads, 0, st, bitmap, p.dim, p.block_size, table, (float)workers, inv,
+              pow2, out, z4, zn4, zc, p.hp, pm);
+}
+
+cudaError_t launch_decode(const Plan& p, const uint32_t* bitmap, const float* table, int workers,
+                          float* out, cudaStream_t st, float* zero_table, unsigned long long* zero_counters,
+                          const PeerMaps* peers) {
+  PeerMaps pm{};
+  if (peers != nullptr && p.block_size == 1) pm = *peers;
+  switch (p.hp.rows) {
+#define S2_CASE(r) \
+  case r: launch_decode_r<r>(p, bitmap, table, workers, out, zero_table, zero_counters, pm, st); break;
+    S2_CASE(1) S2_CASE(2) S2_CASE(3) S2_CASE(4) S2_CASE(5) S2_CASE(6) S2_CASE(7) S2_CASE(8)
+    S2_CASE(9) S2_CASE(10) S2_CASE(11) S2_CASE(12) S2_CASE(13) S2_CASE(14) S2_CASE(15) S2_CASE(16)
+#undef S2_CASE
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace s2
