@@ -373,7 +373,7 @@ static int64_t layout_p2p(s2_plan* plan, int W, int G) {
   // the table (off by default: the per-tile NVLink latency stalls the decode)
   const char* bd_env = getenv("S2_P2P_BITMAP_IN_DECODE_MAXW");
   const int bd_maxw = bd_env ? atoi(bd_env) : 0;
-  a.table_only = (W <= bd_maxw && plan->p.block_size == 1) ? 1 : 0;
+  a.table_only = (W <= bd_maxw && plan->p.block_size == 1 && (plan->p.hp.rows == 3 || plan->p.hp.rows == 5)) ? 1 : 0;
   for (int k = 0; k < 2; ++k) a.off_tsum[k] = a.oneshot ? take(cells * 4) : a.off_table[k];
   a.cells = cells;
   a.words = words;

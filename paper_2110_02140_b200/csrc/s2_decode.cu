@@ -23,12 +23,15 @@ k_decode(const uint32_t* __restrict__ bitmap, int64_t dim, int64_t bs,
   const int wib = threadIdx.x >> 5;
   const int64_t ntiles = (dim + kTile - 1) / kTile;
   DecodeCtx c{bitmap, table, out, dim, bs, workers, inv_workers, workers_pow2};
-  if (!BLOCKS && pm.n > 0)
-    decode_range_peers<R>(c, pm, (int64_t)blockIdx.x * kWarps + wib, (int64_t)gridDim.x * kWarps, ntiles, hp,
-                          s_q[wib], s_v[wib]);
-  else
-    decode_range<R, BLOCKS>(c, pm, (int64_t)blockIdx.x * kWarps + wib, (int64_t)gridDim.x * kWarps, ntiles, hp,
+  if constexpr (!BLOCKS && (R == 3 || R == 5)) {  // opt-in peer-bitmap path: default row counts only
+    if (pm.n > 0) {
+      decode_range_peers<R>(c, pm, (int64_t)blockIdx.x * kWarps + wib, (int64_t)gridDim.x * kWarps, ntiles, hp,
                             s_q[wib], s_v[wib]);
+      return;
+    }
+  }
+  decode_range<R, BLOCKS>(c, pm, (int64_t)blockIdx.x * kWarps + wib, (int64_t)gridDim.x * kWarps, ntiles, hp,
+                          s_q[wib], s_v[wib]);
 }
 
 template <int R>
