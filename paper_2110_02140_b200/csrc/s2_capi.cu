@@ -385,6 +385,8 @@ static int64_t layout_p2p(s2_plan* plan, int W, int G) {
   a.hier = hv ? atoi(hv) : 0;
   const char* cs = getenv("S2_P2P_COMPRESS_SIGNAL");
   a.csig = cs ? atoi(cs) : 0;
+  const char* pp = getenv("S2_P2P_PIPE");
+  a.pipe = pp ? atoi(pp) : 0;
   return off;
 }
 

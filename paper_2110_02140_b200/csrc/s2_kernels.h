@@ -74,6 +74,7 @@ struct P2PArgs {
   int nvls;                   // 1: reduce in the NVSwitch (multimem.ld_reduce / multimem.st)
   int hier;                   // 1: hierarchical barriers (CTA 0 <-> peers, local release)
   int csig;                   // 1: barrier 1 = poll of the compress-done flags (signal_done)
+  int pipe;                   // 1: pipelined two-shot (per-peer waits, k_p2p_pipe)
   int64_t off_flags_c, off_cdone, off_cepoch;
   unsigned long long* trace;  // optional: per-CTA globaltimer stamps [G][8] (S2_P2P_TRACE=1)
 };

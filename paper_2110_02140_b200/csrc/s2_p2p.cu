@@ -366,6 +366,158 @@ __global__ void __launch_bounds__(kP2PThreads) k_p2p_oneshot(const __grid_consta
   S2_TRACE(4);
 }
 
+// ============================================================ pipelined two-shot
+//
+// Same data movement as k_p2p_aggregate, but every CTA waits for ONE peer at a time:
+// phase A accumulates slice `me` peer by peer (rotation order me+1, me+2, ...) as soon as
+// that peer's CTA b has arrived, phase B copies each peer's reduced slice as soon as that
+// peer's CTA b has finished its phase A — so transfers from early peers overlap the wait
+// for late ones instead of queueing behind two all-peer barriers.  The owner of a slice
+// sums it once and broadcasts it, so every rank still ends with identical tables.
+// Thread 0 spins until at least one peer in `pending` (bit q) has reached `ep` in flag
+// array off_flags, then returns (to the whole CTA) the set of peers ready now.
+template <int W>
+__device__ __forceinline__ uint32_t wait_any(const P2PArgs& a, int64_t off_flags, uint32_t pending, uint32_t ep,
+                                             uint32_t* s_mask) {
+  if (threadIdx.x == 0) {
+    uint32_t ready = 0;
+    uint64_t t0 = 0;
+    for (int spin = 0;; ++spin) {
+#pragma unroll
+      for (int q = 0; q < W; ++q) {
+        if (!((pending >> q) & 1u)) continue;
+        const uint32_t* f = reinterpret_cast<const uint32_t*>(a.base[a.rank] + off_flags) + q * gridDim.x + blockIdx.x;
+        if ((int32_t)(ld_acquire_sys(f) - ep) >= 0) ready |= 1u << q;
+      }
+      if (ready) break;
+      if ((spin & 1023) == 1023) {
+        const uint64_t now = globaltimer();
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > 10000000000ull) {
+          atomicOr(reinterpret_cast<uint32_t*>(a.base[a.rank] + a.off_error), 1u);
+          ready = pending;  // give up waiting; results are flagged as invalid
+          break;
+        }
+      }
+    }
+    *s_mask = ready;
+  }
+  __syncthreads();
+  const uint32_t r = *s_mask;
+  __syncthreads();
+  return r;
+}
+
+template <int W>
+__device__ __forceinline__ void signal_flags(const P2PArgs& a, int64_t off_flags, uint32_t ep) {
+  __syncthreads();  // this CTA's writes happen-before thread q's release (bar.sync is cumulative)
+  if (threadIdx.x < W)
+    st_release_sys(reinterpret_cast<uint32_t*>(a.base[threadIdx.x] + off_flags) + a.rank * gridDim.x + blockIdx.x, ep);
+}
+
+// Same data movement as k_p2p_aggregate, but a CTA never waits for all peers at once:
+// phase A accumulates slice `me` from whichever peers have arrived (all ready peers'
+// loads in flight together), phase B copies each peer's reduced slice chunk as soon as
+// that peer's CTA b has finished its phase A.  The owner of a slice sums it once and
+// broadcasts it, so every rank still ends with identical tables.
+template <int W>
+__global__ void __launch_bounds__(kP2PThreads) k_p2p_pipe(const __grid_constant__ P2PArgs a) {
+  __shared__ uint32_t s_ep, s_mask;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic launch: compress must be complete
+  S2_TRACE(0);
+  if (threadIdx.x == 0) {
+    uint32_t* e = reinterpret_cast<uint32_t*>(a.base[a.rank] + a.off_epoch) + blockIdx.x;
+    s_ep = *e + 1u;
+    *e = s_ep;
+  }
+  __syncthreads();
+  const uint32_t ep = s_ep;
+  const int me = a.rank, cur = a.cur;
+  const int64_t t4 = a.cells / 4 / W;  // 16-byte vectors per slice: table ...
+  const int64_t w4 = a.words / 4 / W;  // ... and bitmap
+  int64_t lo, hi;
+  chunk_of(t4 + w4, lo, hi);
+  signal_flags<W>(a, a.off_flags_a, ep);  // my compress is complete
+  const uint32_t others = ((1u << W) - 1u) & ~(1u << me);
+  constexpr int B = W <= 2 ? 2 : 1;  // register budget (64/thread at 1024 threads)
+  // each thread owns at most B vectors of the chunk per round (rounds only when the chunk is large)
+  for (int64_t r0 = lo; r0 < hi; r0 += (int64_t)B * kP2PThreads) {
+    uint4 acc[B];
+    int64_t off[B];
+    bool tab[B], ok[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      const int64_t i = r0 + threadIdx.x + (int64_t)k * kP2PThreads;
+      ok[k] = i < hi;
+      tab[k] = i < t4;
+      off[k] = tab[k] ? a.off_table[cur] + (me * t4 + i) * 16 : a.off_bitmap[cur] + (me * w4 + i - t4) * 16;
+      if (ok[k]) acc[k] = *reinterpret_cast<const uint4*>(a.base[me] + off[k]);
+    }
+    uint32_t pending = others;
+    while (pending) {
+      const uint32_t ready = wait_any<W>(a, a.off_flags_a, pending, ep, &s_mask);
+      pending &= ~ready;
+      uint4 v[W][B];
+#pragma unroll
+      for (int q = 0; q < W; ++q) {
+        if (!((ready >> q) & 1u)) continue;
+#pragma unroll
+        for (int k = 0; k < B; ++k)
+          if (ok[k]) v[q][k] = __ldcg(reinterpret_cast<const uint4*>(a.base[q] + off[k]));
+      }
+#pragma unroll
+      for (int q = 0; q < W; ++q) {
+        if (!((ready >> q) & 1u)) continue;
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+          if (!ok[k]) continue;
+          if (tab[k]) {
+            acc[k].x = __float_as_uint(__uint_as_float(acc[k].x) + __uint_as_float(v[q][k].x));
+            acc[k].y = __float_as_uint(__uint_as_float(acc[k].y) + __uint_as_float(v[q][k].y));
+            acc[k].z = __float_as_uint(__uint_as_float(acc[k].z) + __uint_as_float(v[q][k].z));
+            acc[k].w = __float_as_uint(__uint_as_float(acc[k].w) + __uint_as_float(v[q][k].w));
+          } else {
+            acc[k].x |= v[q][k].x; acc[k].y |= v[q][k].y; acc[k].z |= v[q][k].z; acc[k].w |= v[q][k].w;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      if (!ok[k]) continue;
+      const int64_t i = r0 + threadIdx.x + (int64_t)k * kP2PThreads;
+      const int64_t dst = tab[k] ? off[k] : a.off_union[cur] + (me * w4 + i - t4) * 16;
+      *reinterpret_cast<uint4*>(a.base[me] + dst) = acc[k];
+    }
+  }
+  S2_TRACE(1);
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // every peer has arrived
+  signal_flags<W>(a, a.off_flags_b, ep);  // my reduced slice chunk is final
+  S2_TRACE(2);
+  uint32_t pending = others;
+  while (pending) {
+    const uint32_t ready = wait_any<W>(a, a.off_flags_b, pending, ep, &s_mask);
+    pending &= ~ready;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += kP2PThreads) {
+      uint4 v[W];
+#pragma unroll
+      for (int q = 0; q < W; ++q) {
+        if (!((ready >> q) & 1u)) continue;
+        const int64_t o = i < t4 ? a.off_table[cur] + (q * t4 + i) * 16 : a.off_union[cur] + (q * w4 + i - t4) * 16;
+        v[q] = __ldcg(reinterpret_cast<const uint4*>(a.base[q] + o));
+      }
+#pragma unroll
+      for (int q = 0; q < W; ++q) {
+        if (!((ready >> q) & 1u)) continue;
+        const int64_t o = i < t4 ? a.off_table[cur] + (q * t4 + i) * 16 : a.off_union[cur] + (q * w4 + i - t4) * 16;
+        *reinterpret_cast<uint4*>(a.base[me] + o) = v[q];
+      }
+    }
+  }
+  __syncthreads();
+  S2_TRACE(4);
+}
+
 // ============================================================ NVLS (in-switch) exchange
 //
 // With torch symmetric memory the arena also has a multicast address: a load-reduce on it
@@ -679,6 +831,17 @@ cudaError_t launch_p2p_aggregate(const P2PArgs& a, int grid, cudaStream_t st) {
       case 6: fn = (const void*)k_nvls_exchange<6>; break;
       case 7: fn = (const void*)k_nvls_exchange<7>; break;
       case 8: fn = (const void*)k_nvls_exchange<8>; break;
+      default: return cudaErrorInvalidValue;
+    }
+  } else if (a.pipe && !a.oneshot) {
+    switch (a.world) {
+      case 2: fn = (const void*)k_p2p_pipe<2>; break;
+      case 3: fn = (const void*)k_p2p_pipe<3>; break;
+      case 4: fn = (const void*)k_p2p_pipe<4>; break;
+      case 5: fn = (const void*)k_p2p_pipe<5>; break;
+      case 6: fn = (const void*)k_p2p_pipe<6>; break;
+      case 7: fn = (const void*)k_p2p_pipe<7>; break;
+      case 8: fn = (const void*)k_p2p_pipe<8>; break;
       default: return cudaErrorInvalidValue;
     }
   } else if (a.oneshot) {

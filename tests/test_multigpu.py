@@ -27,6 +27,7 @@ VARIANTS = {
     "graph": {"S2_CHECK_GRAPH": "1"},          # CUDA-graph replay of the whole reduce
     "hier": {"S2_P2P_HIER": "1"},              # hierarchical cross-rank barriers
     "csig": {"S2_P2P_COMPRESS_SIGNAL": "1"},   # compress kernels signal completion to the peers
+    "pipe": {"S2_P2P_PIPE": "1", "S2_P2P_ONESHOT_MAXW": "1"},  # pipelined two-shot, per-peer waits
 }
 
 
