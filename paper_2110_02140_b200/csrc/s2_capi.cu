@@ -584,6 +584,9 @@ int s2_aggregate(s2_plan* plan, float* table, const uint32_t* bitmap, uint32_t* 
   }
   int rc = ensure_scratch(plan);
   if (rc) return rc;
+  if (!plan->comm) return fail(S2_EINVAL, "s2_aggregate needs an NCCL communicator (s2_comm_init)");
+  if (!plan->gather)  // peer-memory plans skip the NCCL landing buffer until asked
+    S2_CUDA(cudaMalloc(&plan->gather, sizeof(uint32_t) * (size_t)q.words * plan->world), "cudaMalloc(gather)");
   const size_t cells = (size_t)q.hp.rows * q.hp.cols;
   // sketch sum (sketch.py:213-216) and bitmap gather, one NCCL group over NVLink
   S2_NCCL(ncclGroupStart(), "ncclGroupStart");
