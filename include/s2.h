@@ -118,6 +118,7 @@ int s2_selected_count(const s2_plan* plan, const uint32_t* bitmap, uint64_t* cou
 /* BlockMask.selected_indices (sparse.py:44-49) when values == NULL, or the
  * compacted (idx, val) pairs sparse_compress inserts (sparse.py:164-168) when
  * g != NULL: ascending int64 indices (and float32 values), count into *count.
+ * idx_out == NULL only counts (size the outputs, then call again).
  * scratch: device bytes >= s2_compact_scratch_bytes(plan). */
 int64_t s2_compact_scratch_bytes(const s2_plan* plan);
 int s2_compact(const s2_plan* plan, const uint32_t* bitmap, const float* g, int64_t* idx_out,

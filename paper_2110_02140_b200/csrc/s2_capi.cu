@@ -286,8 +286,7 @@ int64_t s2_compact_scratch_bytes(const s2_plan* plan) {
 
 int s2_compact(const s2_plan* plan, const uint32_t* bitmap, const float* g, int64_t* idx_out,
                float* val_out, int64_t* count, void* scratch, void* stream) {
-  if (!plan || !bitmap || !idx_out || !count || !scratch)
-    return fail(S2_EINVAL, "NULL argument to s2_compact");
+  if (!plan || !bitmap || !count || !scratch) return fail(S2_EINVAL, "NULL argument to s2_compact");
   if (g && (reinterpret_cast<uintptr_t>(g) & 15)) return fail(S2_EINVAL, "gradient must be 16-byte aligned");
   S2_CUDA(s2::launch_compact(plan->p, bitmap, g, idx_out, g ? val_out : nullptr, count, scratch,
                              as_stream(stream)),

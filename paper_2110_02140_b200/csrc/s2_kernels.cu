@@ -284,7 +284,8 @@ cudaError_t launch_compact(const Plan& p, const uint32_t* bitmap, const float* g
   const int grid = grid_for(ntiles, 4);
   k_compact_count<<<grid, kThreads, 0, st>>>(bitmap, g, p.dim, p.block_size, tiles);
   k_scan<<<1, 1024, 0, st>>>(tiles, ntiles, count);
-  k_compact_write<<<grid, kThreads, 0, st>>>(bitmap, g, p.dim, p.block_size, tiles, idx_out, val_out);
+  if (idx_out != nullptr)  // idx_out == NULL: count only (size the output first)
+    k_compact_write<<<grid, kThreads, 0, st>>>(bitmap, g, p.dim, p.block_size, tiles, idx_out, val_out);
   return cudaGetLastError();
 }
 

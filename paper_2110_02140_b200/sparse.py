@@ -112,17 +112,19 @@ def _union(masks) -> BlockMask:
 
 
 def _compact(mask: BlockMask, g: torch.Tensor | None):
+    """Ordered compaction on the GPU: a counting pass sizes the outputs exactly, then the write pass."""
     p = mask.partition
     plan = get_plan(p.dim, p.num_blocks, 1, 1, 0)
     dev = mask.words.device
     scratch = torch.empty(int(lib.s2_compact_scratch_bytes(plan.handle)) // 8 + 1, dtype=torch.int64, device=dev)
     count = torch.zeros(1, dtype=torch.int64, device=dev)
-    # upper bound on the output: the selected coordinates
-    idx = torch.empty(p.dim, dtype=torch.int64, device=dev)
-    vals = torch.empty(p.dim, dtype=torch.float32, device=dev) if g is not None else None
+    check(lib.s2_compact(plan.handle, ptr(mask.words), ptr(g), None, None, ptr(count), ptr(scratch), stream_ptr()),
+          "compact(count)")
+    n = int(count.item())
+    idx = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    vals = torch.empty(max(n, 1), dtype=torch.float32, device=dev) if g is not None else None
     check(lib.s2_compact(plan.handle, ptr(mask.words), ptr(g), ptr(idx), ptr(vals), ptr(count), ptr(scratch),
                          stream_ptr()), "compact")
-    n = int(count.item())
     return idx[:n], (vals[:n] if vals is not None else None)
 
 
