@@ -56,7 +56,8 @@ def build(force: bool = False, verbose: bool = True) -> str:
     inc, lib = nccl_dirs()
     objdir = os.path.join(PKG, "build_obj")
     os.makedirs(objdir, exist_ok=True)
-    common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+    extra = os.environ.get("S2_NVCC_FLAGS", "").split()
+    common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *extra,
               "-Xptxas", "-v" if verbose and os.environ.get("S2_PTXAS_V") else "-O3",
               "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc]
 
