@@ -415,12 +415,19 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--ref-budget", type=float, default=120.0, help="max seconds of timed reference steps")
+    ap.add_argument("--alpha", type=float, default=None, help="override the config's non-zero fraction")
+    ap.add_argument("--cols", type=int, default=None, help="override the config's sketch width")
     args = ap.parse_args()
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     if ws != args.gpus and "WORLD_SIZE" in os.environ:
         args.gpus = ws
     args.warmup = max(args.warmup, 3)
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.alpha is not None:
+        cfg["alpha"] = args.alpha
+        cfg["label"] += f" (alpha={args.alpha})"
+    if args.cols is not None:
+        cfg["cols"] = args.cols
     if args.impl == "reference":
         reference_arm(args, cfg)
     else:
