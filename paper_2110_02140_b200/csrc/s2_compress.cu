@@ -696,6 +696,10 @@ static void launch_compress_r(const Plan& p, const float* g, uint32_t* bitmap, f
 cudaError_t launch_compress(const Plan& p, const float* g, uint32_t* bitmap, float* table,
                             unsigned long long* counters, int mode, cudaStream_t st, bool prezeroed, void* list,
                             const DoneSignal* signal) {
+  l2_window() = L2Window{table, sizeof(float) * (size_t)p.hp.rows * p.hp.cols};
+  struct Reset {
+    ~Reset() { l2_window() = L2Window{}; }
+  } reset_window;
   DoneSignal sig{};
   if (signal != nullptr) sig = *signal;
   cudaError_t e = cudaSuccess;

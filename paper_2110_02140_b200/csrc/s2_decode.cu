@@ -54,6 +54,10 @@ static void launch_decode_r(const Plan& p, const uint32_t* bitmap, const float* 
 cudaError_t launch_decode(const Plan& p, const uint32_t* bitmap, const float* table, int workers,
                           float* out, cudaStream_t st, float* zero_table, unsigned long long* zero_counters,
                           const PeerMaps* peers) {
+  l2_window() = L2Window{table, sizeof(float) * (size_t)p.hp.rows * p.hp.cols};
+  struct Reset {
+    ~Reset() { l2_window() = L2Window{}; }
+  } reset_window;
   PeerMaps pm{};
   if (peers != nullptr && p.block_size == 1) pm = *peers;
   switch (p.hp.rows) {

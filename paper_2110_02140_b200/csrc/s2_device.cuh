@@ -45,6 +45,36 @@ inline bool pdl_enabled() {
   return v != 0;
 }
 
+// Optional L2 persistence for the sketch table (S2_L2_PERSIST=1): the table is the only
+// data with reuse (r atomics / gathers per value against a 3-50 MB table) while the
+// gradient and the output stream through once; an access-policy window marks it
+// persisting so the streams cannot evict it.
+struct L2Window {
+  const void* base = nullptr;
+  size_t bytes = 0;
+};
+inline L2Window& l2_window() {
+  static thread_local L2Window w;
+  return w;
+}
+inline bool l2_persist_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("S2_L2_PERSIST");
+    v = e ? atoi(e) : 0;
+    if (v) {
+      int dev = 0, maxp = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+      if (maxp <= 0 || cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp) != cudaSuccess) {
+        cudaGetLastError();
+        v = 0;
+      }
+    }
+  }
+  return v != 0;
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                              Args&&... args) {
@@ -53,11 +83,21 @@ inline cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, si
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  const L2Window& w = l2_window();
+  if (w.base != nullptr && l2_persist_enabled()) {
+    attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[1].val.accessPolicyWindow.base_ptr = const_cast<void*>(w.base);
+    attr[1].val.accessPolicyWindow.num_bytes = w.bytes;
+    attr[1].val.accessPolicyWindow.hitRatio = 1.0f;
+    attr[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.numAttrs = 2;
+  }
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
