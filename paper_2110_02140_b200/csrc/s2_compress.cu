@@ -140,7 +140,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // LOAD 1: the next tile (4 KB) is prefetched into a per-warp shared buffer by one TMA bulk
 //         copy (cp.async.bulk + mbarrier) right after the current tile has been moved to
 //         registers, so prefetch costs no registers and 4 CTAs (32 warps) fit per SM.
-template <int R, int MODE, int LOAD>
+template <int R, int MODE, int LOAD, bool SIG = false>
 __global__ void __launch_bounds__(kThreads, LOAD == 0 ? 2 : 4)
 k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __restrict__ bitmap,
            float* __restrict__ table, unsigned long long* __restrict__ counters,
@@ -347,7 +347,7 @@ k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __res
     if (MODE == 2 && sel) atomicAdd(counters + S2_CNT_SELECTED, sel);
     if (bad) atomicOr(counters + S2_CNT_NONFINITE, 1ull);
   }
-  if (sig.done != nullptr) signal_done(sig);
+  if constexpr (SIG) signal_done(sig);  // separate instantiation: no CTA barrier in the default kernel
 }
 
 // ------------------------------------------- compress, TMA-staged variant (default)
@@ -649,14 +649,26 @@ static void launch_compress_rm(const Plan& p, const float* g, uint32_t* bitmap, 
   }
   const int grid = grid_for(ntiles, waves > 0 ? waves : (LOAD == 0 ? 2 : 4));
   if (mode == S2_MASK_GIVEN) {
-    launch_ex(k_compress<R, 2, LOAD>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table, counters, p.hp,
-              sig);
+    if (sig.done != nullptr)
+      launch_ex(k_compress<R, 2, LOAD, true>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table,
+                counters, p.hp, sig);
+    else
+      launch_ex(k_compress<R, 2, LOAD>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table, counters,
+                p.hp, sig);
   } else if (p.block_size == 1) {
-    launch_ex(k_compress<R, 0, LOAD>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table, counters, p.hp,
-              sig);
+    if (sig.done != nullptr)
+      launch_ex(k_compress<R, 0, LOAD, true>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table,
+                counters, p.hp, sig);
+    else
+      launch_ex(k_compress<R, 0, LOAD>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table, counters,
+                p.hp, sig);
   } else {
-    launch_ex(k_compress<R, 1, LOAD>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table, counters, p.hp,
-              sig);
+    if (sig.done != nullptr)
+      launch_ex(k_compress<R, 1, LOAD, true>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table,
+                counters, p.hp, sig);
+    else
+      launch_ex(k_compress<R, 1, LOAD>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table, counters,
+                p.hp, sig);
   }
 }
 
