@@ -28,6 +28,7 @@ VARIANTS = {
     "hier": {"S2_P2P_HIER": "1"},              # hierarchical cross-rank barriers
     "csig": {"S2_P2P_COMPRESS_SIGNAL": "1"},   # compress kernels signal completion to the peers
     "pipe": {"S2_P2P_PIPE": "1", "S2_P2P_ONESHOT_MAXW": "1"},  # pipelined two-shot, per-peer waits
+    "blocks": {"S2_CHECK_NUM_BLOCKS": "62500"},  # block bitmap (b < d, 32 elements per block)
 }
 
 

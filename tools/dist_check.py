@@ -36,7 +36,8 @@ torch.cuda.set_device(local)
 dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 import paper_2110_02140_b200 as s2  # noqa: E402
 
-red = s2.S2Reducer(a.dim, rows=a.rows, cols=a.cols, seed=0)
+nb = int(os.environ.get("S2_CHECK_NUM_BLOCKS", "0")) or a.dim  # block bitmap (b < d) when set
+red = s2.S2Reducer(a.dim, rows=a.rows, cols=a.cols, seed=0, num_blocks=nb)
 graphed = None
 if os.environ.get("S2_CHECK_GRAPH") == "1":  # replay captured CUDA graphs instead of direct calls
     from paper_2110_02140_b200.reducer import GraphedReduce
@@ -53,17 +54,18 @@ for kind in ("int", "normal"):
         else:
             g_static.copy_(torch.from_numpy(grads[rank]))
             out = graphed().cpu().numpy()
-    ps = [o.compress(g, g != 0, a.rows, a.cols, 0) for g in grads]
+    ps = [o.compress(g, o.nonzero_flags(g, nb), a.rows, a.cols, 0) for g in grads]
     m = o.merge(ps)
     ref = o.decompress(m)
     if kind == "int":
         ok = bool(np.array_equal(out, ref.astype(np.float32)))
         err = float(np.abs(out - ref).max())
     else:
-        union = np.flatnonzero(m.flags)
+        union = o.selected_indices(m.flags, a.dim)
         mass = np.zeros((a.rows, a.cols))
         for g, p in zip(grads, ps):
-            idx = np.flatnonzero(p.flags)
+            idx = o.selected_indices(p.flags, a.dim)
+            idx = idx[g[idx] != 0]
             mass += o.sketch_l1_mass(o.row_seeds(0, a.rows), idx, g[idx].astype(np.float64), a.cols)
         mmax = np.zeros(union.size)
         for j, s in enumerate(o.row_seeds(0, a.rows)):
