@@ -12,8 +12,8 @@ N * 4*d / t_reduce (t = max over ranks, CUDA events, K steps); ``ms_per_step``
 = t_reduce.  ``e2e`` repeats the measurement through the same C-ABI call with
 pinned HOST buffers, H2D of the gradient and D2H of the result inside the timed
 region.  ``--impl reference`` times the CPU reference path (the NumPy oracle
-port of sketchgrad.sparse, bit-identical to the as-shipped reference) on the
-host cores instead.
+port of sketchgrad.sparse, bit-identical to the as-shipped reference) on all the
+host cores instead (oracle/parallel.py).
 """
 
 from __future__ import annotations
@@ -129,92 +129,70 @@ class ClockSampler:
 # ----------------------------------------------------------------- reference
 
 
-def reference_arm(args, cfg):
-    """CPU reference: oracle port of sketchgrad.sparse (compress per rank in W processes,
-    merge, decompress), on the host cores.  Rank 0 only under torchrun."""
+def _host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def _ref_grads(cfg, W):
     from oracle import s2_oracle as o
 
+    return [o.synthetic_gradient(cfg["dim"], cfg["alpha"], r) if cfg.get("grid") is None
+            else _rows_gradient_np(cfg, r) for r in range(W)]
+
+
+def _time_reference(cfg, W, warmup, max_steps, budget_s):
+    """Oracle port of sketchgrad.sparse on every host core (oracle/parallel.py): W ranks'
+    compress, merge, decompress per step.  Returns (s/step, steps, cores)."""
+    from oracle.parallel import ParallelReference
+
+    pr = ParallelReference(_ref_grads(cfg, W), cfg["rows"], cfg["cols"], 0, procs=_host_cores(),
+                           num_blocks=cfg.get("num_blocks", cfg["dim"]))
+    try:
+        for _ in range(warmup):
+            pr.step()
+        t0, done = time.perf_counter(), 0
+        while done < max_steps:
+            pr.step()
+            done += 1
+            if time.perf_counter() - t0 > budget_s and done >= 3:
+                break  # bounded sample: the run must finish within a few minutes
+        return (time.perf_counter() - t0) / done, done, pr.procs
+    finally:
+        pr.close()
+
+
+def reference_arm(args, cfg):
+    """CPU reference on the host cores, rank 0 only under torchrun."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     W = args.gpus
-    d, rows, cols = cfg["dim"], cfg["rows"], cfg["cols"]
-    nb = cfg.get("num_blocks", d)
-    grads = [o.synthetic_gradient(d, cfg["alpha"], r) if cfg.get("grid") is None else _rows_gradient_np(cfg, r)
-             for r in range(W)]
-
-    def one_step(pool):
-        if pool is None:
-            ps = [o.compress(grads[0], o.nonzero_flags(grads[0], nb), rows, cols, 0)]
-        else:
-            ps = pool.map(_ref_compress, [(r, rows, cols, nb) for r in range(W)])
-        m = o.merge(ps)
-        return o.decompress(m)
-
-    pool = None
-    if W > 1:
-        import multiprocessing as mp
-
-        global _REF_GRADS
-        _REF_GRADS = grads
-        pool = mp.get_context("fork").Pool(W)
-    for _ in range(args.warmup):
-        one_step(pool)
-    t0 = time.perf_counter()
-    done = 0
-    while done < args.steps:
-        one_step(pool)
-        done += 1
-        if time.perf_counter() - t0 > args.ref_budget and done >= 3:
-            break  # bounded sample: the run must finish within a few minutes
-    dt = (time.perf_counter() - t0) / done
-    if pool is not None:
-        pool.close()
+    d = cfg["dim"]
+    dt, done, cores = _time_reference(cfg, W, args.warmup, args.steps, args.ref_budget)
     value = W * 4 * d / dt / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": W,
         "steps": done, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": _config_json(args, cfg),
-        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": W, "kind": "port",
-                         "sample": f"full workload per step: {W} rank compress (one process each) + merge + "
-                                   f"decompress of {d} elements; numpy {np.__version__}; host has "
-                                   f"{os.cpu_count()} cores"},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": "port",
+                         "sample": f"full workload per step: {W} ranks' compress + merge + decompress of "
+                                   f"{d} elements each, chunked over {cores} worker processes "
+                                   f"(oracle/parallel.py); numpy {np.__version__}"},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-_REF_GRADS = None
-
-
-def _ref_compress(a):
-    from oracle import s2_oracle as o
-
-    r, rows, cols, nb = a
-    g = _REF_GRADS[r]
-    return o.compress(g, o.nonzero_flags(g, nb), rows, cols, 0)
-
-
 def cpu_baseline(cfg, budget_s=10.0):
-    """Oracle port timed on this host (rank 0, N=1): compress + merge + decompress of one gradient."""
-    from oracle import s2_oracle as o
-
-    d = cfg["dim"]
-    g = o.synthetic_gradient(d, cfg["alpha"], 0) if cfg.get("grid") is None else \
-        _rows_gradient_np(cfg)
-    nb = cfg.get("num_blocks", d)
-    n, t0 = 0, time.perf_counter()
-    while True:
-        p = o.compress(g, o.nonzero_flags(g, nb), cfg["rows"], cfg["cols"], 0)
-        o.decompress(o.merge([p]))
-        n += 1
-        if time.perf_counter() - t0 > budget_s or n >= 50:
-            break
-    dt = (time.perf_counter() - t0) / n
-    return {"value": round(4 * d / dt / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "port",
-            "sample": f"{n} full reduces (W=1) of the {d}-element workload in {time.perf_counter() - t0:.1f}s; "
-                      f"numpy {np.__version__} single-threaded; host has {os.cpu_count()} cores"}
+    """Oracle port timed on this host's cores (rank 0, N=1): compress + merge + decompress of one gradient."""
+    dt, n, cores = _time_reference(cfg, 1, 1, 50, budget_s)
+    return {"value": round(4 * cfg["dim"] / dt / 1e9, 4), "unit": "GB/s", "cores": cores, "kind": "port",
+            "sample": f"{n} full reduces (W=1) of the {cfg['dim']}-element workload, chunked over {cores} "
+                      f"worker processes (oracle/parallel.py); numpy {np.__version__}"}
 
 
 def _rows_gradient_np(cfg, rank=0):

@@ -151,3 +151,20 @@ def test_bench_generator_matches_oracle_recipe():
 
     for d, a, r in ((10_000, 0.01, 0), (100_003, 0.05, 3)):
         assert np.array_equal(synthetic.numpy_gradient(d, a, r), o.synthetic_gradient(d, a, r))
+
+
+@pytest.mark.parametrize("d,nb,W", [(50_003, 50_003, 1), (50_003, 50_003, 3), (40_000, 400, 2)])
+def test_parallel_reference_matches_oracle(d, nb, W):
+    """bench.py's reference arm (oracle/parallel.py, chunked over worker processes) computes the
+    oracle's reduce; on small-integer inputs the float64 sums are exact in any order."""
+    from oracle.parallel import ParallelReference
+
+    gs = [o.synthetic_gradient(d, 0.02, r, kind="int") for r in range(W)]
+    _, ref = o.reduce(gs, nb, 3, 512, 7)
+    pr = ParallelReference(gs, 3, 512, 7, procs=3, num_blocks=nb)
+    try:
+        for _ in range(2):  # second step reuses the shared buffers
+            out = pr.step().copy()
+            assert np.array_equal(out, ref)
+    finally:
+        pr.close()
