@@ -41,6 +41,9 @@ CONFIGS = {
                  label="LSTM-LM embedding 200M fp32 (200k x 1000), 99.9% row-sparse, element bitmap"),
     "lstm_rows": dict(dim=200_000_000, alpha=0.001, rows=3, cols=1_048_576, grid=(200_000, 1_000),
                       num_blocks=200_000, label="LSTM-LM embedding 200M, 99.9% row-sparse, row bitmap (b=200k)"),
+    "lstm_rows_zipf": dict(dim=200_000_000, alpha=0.001, rows=3, cols=1_048_576, grid=(200_000, 1_000),
+                           num_blocks=200_000, zipf=1.1,
+                           label="LSTM-LM embedding 200M, 99.9% Zipf(1.1) rows (ranks overlap), row bitmap"),
     "gpt2m_90": dict(dim=355_000_000, alpha=0.10, rows=3, cols=1_048_576, label="GPT-2-medium 355M, 90% sparse"),
     "gpt2m_99": dict(dim=355_000_000, alpha=0.01, rows=3, cols=1_048_576, label="GPT-2-medium 355M, 99% sparse"),
     "gpt2m_999": dict(dim=355_000_000, alpha=0.001, rows=3, cols=262_144, label="GPT-2-medium 355M, 99.9% sparse"),
@@ -198,7 +201,12 @@ def cpu_baseline(cfg, budget_s=10.0):
 def _rows_gradient_np(cfg, rank=0):
     V, H = cfg["grid"]
     rng = np.random.default_rng(1234 + rank)
-    r = rng.choice(V, max(1, int(round(cfg["alpha"] * V))), replace=False)
+    p = None
+    if cfg.get("zipf"):
+        from paper_2110_02140_b200.synthetic import zipf_weights
+
+        p = zipf_weights(V, cfg["zipf"])
+    r = rng.choice(V, max(1, int(round(cfg["alpha"] * V))), replace=False, p=p)
     g = np.zeros(cfg["dim"], dtype=np.float32)
     for row in r:
         g[row * H:(row + 1) * H] = rng.standard_normal(H).astype(np.float32)
@@ -235,7 +243,7 @@ def ours(args, cfg):
 
     d, rows, cols = cfg["dim"], cfg["rows"], cfg["cols"]
     red = s2.S2Reducer(d, rows=rows, cols=cols, seed=0, world=world, rank=rank, num_blocks=cfg.get("num_blocks"))
-    gcfg = dict(dim=d, alpha=cfg["alpha"], rows=cfg.get("grid"))
+    gcfg = dict(dim=d, alpha=cfg["alpha"], rows=cfg.get("grid"), zipf=cfg.get("zipf"))
     n_rot = N_ROTATE if d <= 50_000_000 else 2  # 2 x >= 440 MB still exceeds the 126 MB L2
     grads = [synthetic.gradient(gcfg, rank, base_seed=1234 + 1000 * k) for k in range(n_rot)]
     outs = [torch.empty(d, dtype=torch.float32, device="cuda") for _ in range(n_rot)]
@@ -328,6 +336,26 @@ def ours(args, cfg):
     torch.cuda.synchronize()
     ms_e2e = max_over_ranks(e0.elapsed_time(e1) / ke)
     barrier()
+
+    # side-by-side: dense NCCL all-reduce of the same fp32 gradient, the
+    # uncompressed exchange a DDP step would do instead of the sparse-sketch reduce
+    dense = None
+    if world > 1:
+        buf = grads[0].clone()
+        kd = max(5, min(args.steps, 50))
+        for _ in range(5):
+            dist.all_reduce(buf)
+        barrier()
+        e0.record(stream)
+        for _ in range(kd):
+            dist.all_reduce(buf)
+        e1.record(stream)
+        barrier()
+        ms_dense = max_over_ranks(e0.elapsed_time(e1) / kd)
+        dense = {"ms_per_step": round(ms_dense, 5), "value": round(world * B / (ms_dense * 1e-3) / 1e9, 2),
+                 "unit": "GB/s", "op": f"torch.distributed.all_reduce (NCCL, SUM) of {d} fp32, device-resident"}
+        del buf
+    barrier()
     clocks.mark("load_end")
     clk = clocks.stop()
 
@@ -376,6 +404,8 @@ def ours(args, cfg):
         "gpu_launches": args.steps * (3 if world > 1 else 2),
         "clocks": clk,
     }
+    if dense is not None:
+        line["dense_allreduce"] = dense
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_budget)
     print(json.dumps(line), flush=True)

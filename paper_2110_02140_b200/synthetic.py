@@ -24,10 +24,16 @@ def numpy_gradient(dim: int, alpha: float, rank: int = 0, base_seed: int = 1234)
     return g
 
 
+def zipf_weights(V: int, s: float) -> np.ndarray:
+    """Row-draw probabilities p_i ~ 1/(i+1)^s: a vocabulary sorted by frequency, so ranks' rows overlap."""
+    w = 1.0 / np.arange(1, V + 1, dtype=np.float64) ** s
+    return w / w.sum()
+
+
 def cuda_gradient(dim: int, alpha: float, rank: int = 0, base_seed: int = 1234, rows: tuple | None = None,
-                  device="cuda"):
+                  device="cuda", zipf: float | None = None):
     """fp32 CUDA gradient with round(alpha*dim) non-zeros at distinct random positions, or (rows=(V, H))
-    round(alpha*V) full non-zero rows of a V x H row-major matrix."""
+    round(alpha*V) full non-zero rows of a V x H row-major matrix (uniform rows, or Zipf(zipf) rows)."""
     import torch
 
     gen = torch.Generator(device=device)
@@ -36,7 +42,11 @@ def cuda_gradient(dim: int, alpha: float, rank: int = 0, base_seed: int = 1234, 
     if rows is not None:
         V, H = rows
         k = max(1, int(round(alpha * V)))
-        r = torch.randperm(V, generator=gen, device=device)[:k]
+        if zipf:
+            w = torch.from_numpy(zipf_weights(V, zipf)).to(device)
+            r = torch.multinomial(w, k, replacement=False, generator=gen)
+        else:
+            r = torch.randperm(V, generator=gen, device=device)[:k]
         idx = (r[:, None] * H + torch.arange(H, device=device)[None, :]).reshape(-1)
     else:
         k = int(round(alpha * dim))
@@ -53,4 +63,5 @@ def gradient(cfg: dict, rank: int = 0, base_seed: int = 1234, device="cuda"):
 
     if cfg.get("rows") is None and cfg["dim"] <= 50_000_000:
         return torch.from_numpy(numpy_gradient(cfg["dim"], cfg["alpha"], rank, base_seed)).to(device)
-    return cuda_gradient(cfg["dim"], cfg["alpha"], rank, base_seed, rows=cfg.get("rows"), device=device)
+    return cuda_gradient(cfg["dim"], cfg["alpha"], rank, base_seed, rows=cfg.get("rows"), device=device,
+                         zipf=cfg.get("zipf"))
