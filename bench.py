@@ -352,7 +352,7 @@ def ours(args, cfg):
         e1.record(stream)
         barrier()
         ms_dense = max_over_ranks(e0.elapsed_time(e1) / kd)
-        dense = {"ms_per_step": round(ms_dense, 5), "value": round(world * B / (ms_dense * 1e-3) / 1e9, 2),
+        dense = {"ms_per_step": round(ms_dense, 5), "value": round(world * 4 * d / (ms_dense * 1e-3) / 1e9, 2),
                  "unit": "GB/s", "op": f"torch.distributed.all_reduce (NCCL, SUM) of {d} fp32, device-resident"}
         del buf
     barrier()
