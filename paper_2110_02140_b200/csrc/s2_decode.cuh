@@ -98,10 +98,6 @@ __device__ __forceinline__ void zero_next(float4* __restrict__ zt, int64_t zt_n4
   if (zc != nullptr && blockIdx.x == 0 && threadIdx.x < S2_NUM_COUNTERS) zc[threadIdx.x] = 0ull;
 }
 
-// Decode warp tiles t0, t0+tstep, ... < tend (one warp).  Per tile: the bitmap word is
-// prefetched one tile ahead, set positions are compacted by a warp scan into q, values
-// (r gathers + lower median + IEEE /W) land in vals, and the tile is written as dense
-// float4 streaming stores (zeros included).
 // Decode one warp tile (1024 elements at `base`) given its 32 union words (one per lane):
 // set positions are compacted by a warp scan into q, values (r gathers + lower median +
 // IEEE /W) land in vals, and the tile is written as dense float4 streaming stores.
