@@ -373,6 +373,16 @@ static int64_t layout_p2p(s2_plan* plan, int W, int G) {
   const char* bd_env = getenv("S2_P2P_BITMAP_IN_DECODE_MAXW");
   const int bd_maxw = bd_env ? atoi(bd_env) : 0;
   a.table_only = (W <= bd_maxw && plan->p.block_size == 1 && (plan->p.hp.rows == 3 || plan->p.hp.rows == 5)) ? 1 : 0;
+  // optional: each compress also stores its bitmap words into every peer's inbox (remote NVLink
+  // stores hidden under the gradient stream), the exchange moves only the table and the decode
+  // ORs the W bitmaps from LOCAL memory
+  const char* bp_env = getenv("S2_P2P_BITMAP_PUSH_MAXW");
+  const int bp_maxw = bp_env ? atoi(bp_env) : 0;
+  a.push = (!a.table_only && W <= bp_maxw && plan->p.block_size == 1) ? 1 : 0;
+  for (int k = 0; k < 2; ++k) a.off_inbox[k] = a.push ? take((int64_t)W * words * 4) : -1;
+  // one-shot: the exchange ORs the pushed (local) bitmaps into the union itself;
+  // two-shot: the exchange moves only the table and the decode ORs the local copies
+  if (a.push && !a.oneshot) a.table_only = 1;
   for (int k = 0; k < 2; ++k) a.off_tsum[k] = a.oneshot ? take(cells * 4) : a.off_table[k];
   a.cells = cells;
   a.words = words;
@@ -412,7 +422,7 @@ static int finish_p2p(s2_plan* plan, int G) {
   }
   plan->fused = false;
   const char* fz = getenv("S2_FUSED");
-  if (fz && atoi(fz) != 0 && plan->p.block_size == 1 && !a.nvls) {  // opt-in
+  if (fz && atoi(fz) != 0 && plan->p.block_size == 1 && !a.nvls && !a.push) {  // opt-in
     cudaError_t e = s2::xdecode_grid(plan->p.hp, W, a.oneshot, &plan->x_grid);
     if (e == cudaSuccess && plan->x_grid > 0) plan->fused = true;
     else cudaGetLastError();
@@ -514,6 +524,10 @@ int s2_comm_attach(s2_plan* plan, const uint64_t* bases, int world, uint64_t mc_
   a.mc = reinterpret_cast<char*>(mc_base);
   const char* nv = getenv("S2_NVLS");
   a.nvls = (mc_base != 0 && !(nv && atoi(nv) == 0)) ? 1 : 0;
+  if (a.nvls && a.push) {  // the in-switch exchange reduces the bitmaps itself
+    a.push = 0;
+    a.table_only = 0;
+  }
   S2_CUDA(cudaMemset(plan->arena, 0, bytes), "cudaMemset(arena)");
   return finish_p2p(plan, G);
 }
@@ -612,7 +626,20 @@ int s2_reduce(s2_plan* plan, const float* g, float* out, uint64_t* counters, voi
   unsigned long long* cnt = counters ? reinterpret_cast<unsigned long long*>(counters) : plan->counters[cur];
   if (plan->ev[0]) cudaEventRecord(plan->ev[0], st);
   s2::DoneSignal sig{};
-  const bool use_sig = plan->world > 1 && plan->p2p && plan->pa.csig && !plan->pa.nvls && !plan->fused;
+  const bool use_push = plan->world > 1 && plan->p2p && plan->pa.push && !plan->pa.nvls && !plan->fused;
+  const bool use_sig = plan->world > 1 && plan->p2p && plan->pa.csig && !plan->pa.nvls && !plan->fused && !use_push;
+  s2::BitmapPush push{};
+  if (use_push) {  // slot [rank] of every peer's inbox[cur]
+    const int64_t slot = plan->pa.off_inbox[cur] + (int64_t)plan->rank * plan->pa.words * 4;
+    for (int q = 0; q < plan->world; ++q)
+      if (q != plan->rank) push.dst[push.n++] = reinterpret_cast<uint32_t*>(plan->pa.base[q] + slot);
+    static int fence = -1;
+    if (fence < 0) {
+      const char* f = getenv("S2_P2P_PUSH_FENCE");
+      fence = f ? atoi(f) : 1;
+    }
+    push.fence = fence;
+  }
   if (use_sig) {
     sig.done = reinterpret_cast<unsigned int*>(plan->arena + plan->pa.off_cdone);
     sig.epoch = reinterpret_cast<unsigned int*>(plan->arena + plan->pa.off_cepoch);
@@ -622,7 +649,8 @@ int s2_reduce(s2_plan* plan, const float* g, float* out, uint64_t* counters, voi
     sig.rank = plan->rank;
   }
   S2_CUDA(s2::launch_compress(plan->p, g, bitmap, table, cnt, S2_MASK_NONZERO, st, counters == nullptr,
-                              use_sig ? nullptr : split_list(plan), use_sig ? &sig : nullptr),
+                              (use_sig || use_push) ? nullptr : split_list(plan), use_sig ? &sig : nullptr,
+                              use_push ? &push : nullptr),
           "s2_reduce/compress");
   if (plan->ev[1]) cudaEventRecord(plan->ev[1], st);
   const uint32_t* un = bitmap;
@@ -662,7 +690,10 @@ int s2_reduce(s2_plan* plan, const float* g, float* out, uint64_t* counters, voi
   if (plan->p2p && plan->pa.table_only) {
     pm.n = plan->world;
     for (int q = 0; q < plan->world; ++q)
-      pm.p[q] = reinterpret_cast<const uint32_t*>(plan->pa.base[q] + plan->pa.off_bitmap[cur]);
+      pm.p[q] = reinterpret_cast<const uint32_t*>(
+          q == plan->rank || !plan->pa.push
+              ? plan->pa.base[q] + plan->pa.off_bitmap[cur]                                    // peer memory (NVLink)
+              : plan->arena + plan->pa.off_inbox[cur] + (int64_t)q * plan->pa.words * 4);  // pushed copy, local
   }
   S2_CUDA(s2::launch_decode(plan->p, un, table, plan->world, out, st, plan->tables[nxt], plan->counters[nxt],
                             pm.n ? &pm : nullptr),

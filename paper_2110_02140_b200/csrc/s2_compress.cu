@@ -140,11 +140,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // LOAD 1: the next tile (4 KB) is prefetched into a per-warp shared buffer by one TMA bulk
 //         copy (cp.async.bulk + mbarrier) right after the current tile has been moved to
 //         registers, so prefetch costs no registers and 4 CTAs (32 warps) fit per SM.
-template <int R, int MODE, int LOAD, bool SIG = false>
+// PUSH (MODE 0): every bitmap word is also stored into the peers' inbox slots (BitmapPush),
+//         so the exchange kernel only has to move the sketch table.
+template <int R, int MODE, int LOAD, bool SIG = false, bool PUSH = false>
 __global__ void __launch_bounds__(kThreads, LOAD == 0 ? 2 : 4)
 k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __restrict__ bitmap,
            float* __restrict__ table, unsigned long long* __restrict__ counters,
-           const __grid_constant__ HashParams hp, const __grid_constant__ DoneSignal sig) {
+           const __grid_constant__ HashParams hp, const __grid_constant__ DoneSignal sig,
+           const __grid_constant__ BitmapPush push) {
   constexpr int kCap = 32 + kQFast;
   __shared__ uint32_t s_qi[kWarps][kCap];
   __shared__ float s_qv[kWarps][kCap];
@@ -312,7 +315,14 @@ k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __res
     }
     if (MODE == 0) {
       const int64_t wi = t * 32 + lane;
-      if (wi < nelem_words) bitmap[wi] = word;
+      if (wi < nelem_words) {
+        bitmap[wi] = word;
+        if constexpr (PUSH) {
+#pragma unroll
+          for (int q = 0; q < kMaxWorld; ++q)
+            if (q < push.n) push.dst[q][wi] = word;
+        }
+      }
     } else if (MODE == 1) {
       if (word) {  // OR the flags of every block this 32-element span touches
         const int64_t e0 = base + 32 * lane;
@@ -346,6 +356,14 @@ k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __res
     if (MODE == 0 && nnz) atomicAdd(counters + S2_CNT_SELECTED, nnz);
     if (MODE == 2 && sel) atomicAdd(counters + S2_CNT_SELECTED, sel);
     if (bad) atomicOr(counters + S2_CNT_NONFINITE, 1ull);
+  }
+  if constexpr (PUSH) {  // pushed words performed at system scope before the kernel ends
+    if (push.fence == 1) {
+      __threadfence_system();
+    } else if (push.fence == 2) {
+      __syncwarp();
+      if (lane == 0) __threadfence_system();
+    }
   }
   if constexpr (SIG) signal_done(sig);  // separate instantiation: no CTA barrier in the default kernel
 }
@@ -640,7 +658,8 @@ static int compress_variant() {
 
 template <int R, int LOAD>
 static void launch_compress_rm(const Plan& p, const float* g, uint32_t* bitmap, float* table,
-                               unsigned long long* counters, int mode, cudaStream_t st, const DoneSignal& sig) {
+                               unsigned long long* counters, int mode, cudaStream_t st, const DoneSignal& sig,
+                               const BitmapPush& push) {
   const int64_t ntiles = (p.dim + kTile - 1) / kTile;
   static int waves = -1;  // S2_COMPRESS_CTAS_PER_SM: grid = SMs x this (>= resident -> extra waves)
   if (waves < 0) {
@@ -651,24 +670,27 @@ static void launch_compress_rm(const Plan& p, const float* g, uint32_t* bitmap, 
   if (mode == S2_MASK_GIVEN) {
     if (sig.done != nullptr)
       launch_ex(k_compress<R, 2, LOAD, true>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table,
-                counters, p.hp, sig);
+                counters, p.hp, sig, push);
     else
       launch_ex(k_compress<R, 2, LOAD>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table, counters,
-                p.hp, sig);
+                p.hp, sig, push);
   } else if (p.block_size == 1) {
-    if (sig.done != nullptr)
+    if (push.n > 0)
+      launch_ex(k_compress<R, 0, LOAD, false, true>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table,
+                counters, p.hp, sig, push);
+    else if (sig.done != nullptr)
       launch_ex(k_compress<R, 0, LOAD, true>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table,
-                counters, p.hp, sig);
+                counters, p.hp, sig, push);
     else
       launch_ex(k_compress<R, 0, LOAD>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table, counters,
-                p.hp, sig);
+                p.hp, sig, push);
   } else {
     if (sig.done != nullptr)
       launch_ex(k_compress<R, 1, LOAD, true>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table,
-                counters, p.hp, sig);
+                counters, p.hp, sig, push);
     else
       launch_ex(k_compress<R, 1, LOAD>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table, counters,
-                p.hp, sig);
+                p.hp, sig, push);
   }
 }
 
@@ -690,30 +712,33 @@ static void launch_compress_tma(const Plan& p, const float* g, uint32_t* bitmap,
 
 template <int R>
 static void launch_compress_r(const Plan& p, const float* g, uint32_t* bitmap, float* table,
-                              unsigned long long* counters, int mode, cudaStream_t st, const DoneSignal& sig) {
+                              unsigned long long* counters, int mode, cudaStream_t st, const DoneSignal& sig,
+                              const BitmapPush& push) {
   // the experimental load variants are instantiated for the default row count only
-  const int v = (sig.done != nullptr || R != 3) ? 0 : compress_variant();
+  const int v = (sig.done != nullptr || push.n > 0 || R != 3) ? 0 : compress_variant();
   if constexpr (R == 3) {
-    if (v == 3) return launch_compress_rm<R, 3>(p, g, bitmap, table, counters, mode, st, sig);
-    if (v == 1) return launch_compress_rm<R, 1>(p, g, bitmap, table, counters, mode, st, sig);
+    if (v == 3) return launch_compress_rm<R, 3>(p, g, bitmap, table, counters, mode, st, sig, push);
+    if (v == 1) return launch_compress_rm<R, 1>(p, g, bitmap, table, counters, mode, st, sig, push);
     if (v == 2) {
       if (mode == S2_MASK_GIVEN) return launch_compress_tma<R, 2>(p, g, bitmap, table, counters, st);
       if (p.block_size == 1) return launch_compress_tma<R, 0>(p, g, bitmap, table, counters, st);
       return launch_compress_tma<R, 1>(p, g, bitmap, table, counters, st);
     }
   }
-  launch_compress_rm<R, 0>(p, g, bitmap, table, counters, mode, st, sig);
+  launch_compress_rm<R, 0>(p, g, bitmap, table, counters, mode, st, sig, push);
 }
 
 cudaError_t launch_compress(const Plan& p, const float* g, uint32_t* bitmap, float* table,
                             unsigned long long* counters, int mode, cudaStream_t st, bool prezeroed, void* list,
-                            const DoneSignal* signal) {
+                            const DoneSignal* signal, const BitmapPush* bpush) {
   l2_window() = L2Window{table, sizeof(float) * (size_t)p.hp.rows * p.hp.cols};
   struct Reset {
     ~Reset() { l2_window() = L2Window{}; }
   } reset_window;
   DoneSignal sig{};
   if (signal != nullptr) sig = *signal;
+  BitmapPush push{};
+  if (bpush != nullptr && mode == S2_MASK_NONZERO && p.block_size == 1) push = *bpush;
   cudaError_t e = cudaSuccess;
   if (!prezeroed) {
     e = cudaMemsetAsync(table, 0, sizeof(float) * (size_t)p.hp.rows * p.hp.cols, st);
@@ -725,7 +750,7 @@ cudaError_t launch_compress(const Plan& p, const float* g, uint32_t* bitmap, flo
     e = cudaMemsetAsync(bitmap, 0, sizeof(uint32_t) * (size_t)p.words, st);
     if (e != cudaSuccess) return e;
   }
-  if (list != nullptr && mode == S2_MASK_NONZERO && p.block_size == 1 && sig.done == nullptr) {
+  if (list != nullptr && mode == S2_MASK_NONZERO && p.block_size == 1 && sig.done == nullptr && push.n == 0) {
     const int64_t ntiles = (p.dim + kTile - 1) / kTile;
     e = launch_ex(k_scan_compact, (int)((ntiles + kWarps - 1) / kWarps), kThreads, 0, st, g, p.dim, bitmap,
                   reinterpret_cast<uint2*>(list), counters);
@@ -742,10 +767,10 @@ cudaError_t launch_compress(const Plan& p, const float* g, uint32_t* bitmap, flo
     return cudaGetLastError();
   }
   switch (p.hp.rows) {
-    case 1: launch_compress_r<1>(p, g, bitmap, table, counters, mode, st, sig); break;
-    case 3: launch_compress_r<3>(p, g, bitmap, table, counters, mode, st, sig); break;
-    case 5: launch_compress_r<5>(p, g, bitmap, table, counters, mode, st, sig); break;
-    default: launch_compress_r<0>(p, g, bitmap, table, counters, mode, st, sig); break;
+    case 1: launch_compress_r<1>(p, g, bitmap, table, counters, mode, st, sig, push); break;
+    case 3: launch_compress_r<3>(p, g, bitmap, table, counters, mode, st, sig, push); break;
+    case 5: launch_compress_r<5>(p, g, bitmap, table, counters, mode, st, sig, push); break;
+    default: launch_compress_r<0>(p, g, bitmap, table, counters, mode, st, sig, push); break;
   }
   if (mode == S2_MASK_NONZERO && p.block_size > 1) {
     e = cudaGetLastError();

@@ -26,11 +26,18 @@ struct DoneSignal {  // see signal_done (s2_kernels.cu); done == nullptr: no sig
   uint32_t* peer_flags[kMaxWorldSig];
   int world, rank;
 };
+constexpr int kMaxWorld = 8;
+// element bitmap words also stored straight into each peer's inbox slot for this rank
+// (remote NVLink stores during the compress); n = 0: none
+struct BitmapPush {
+  uint32_t* dst[kMaxWorld];
+  int n;
+  int fence;  // end-of-kernel system fence: 1 every thread, 2 one lane per warp (after __syncwarp)
+};
 cudaError_t launch_compress(const Plan& p, const float* g, uint32_t* bitmap, float* table,
                             unsigned long long* counters, int mode, cudaStream_t st, bool prezeroed = false,
                             void* list = nullptr,  // list: dim x 8 B scratch -> split K1 + K2 path
-                            const DoneSignal* signal = nullptr);
-constexpr int kMaxWorld = 8;
+                            const DoneSignal* signal = nullptr, const BitmapPush* push = nullptr);
 // bitmaps of every rank (peer-mapped) whose OR the decode reads directly; n = 0: use `bitmap`
 struct PeerMaps {
   const uint32_t* p[kMaxWorld];
@@ -76,6 +83,8 @@ struct P2PArgs {
   int csig;                   // 1: barrier 1 = poll of the compress-done flags (signal_done)
   int pipe;                   // 1: pipelined two-shot (per-peer waits, k_p2p_pipe)
   int64_t off_flags_c, off_cdone, off_cepoch;
+  int64_t off_inbox[2];       // bitmap push: W slots of `words` words (slot q = rank q's bitmap), or -1
+  int push;                   // 1: compress pushes its bitmap into the peers' inboxes (table-only exchange)
   unsigned long long* trace;  // optional: per-CTA globaltimer stamps [G][8] (S2_P2P_TRACE=1)
 };
 cudaError_t launch_p2p_aggregate(const P2PArgs& a, int grid, cudaStream_t st);

@@ -331,9 +331,18 @@ __global__ void __launch_bounds__(kP2PThreads) k_p2p_oneshot(const __grid_consta
     for (int k = 0; k < B; ++k) {
       const int64_t i = i0 + (int64_t)k * kP2PThreads;
       if (i < hi) {
-        const int64_t off = i < t4 ? a.off_table[cur] + i * 16 : a.off_bitmap[cur] + (i - t4) * 16;
+        if (i < t4 || !a.push) {
+          const int64_t off = i < t4 ? a.off_table[cur] + i * 16 : a.off_bitmap[cur] + (i - t4) * 16;
 #pragma unroll
-        for (int q = 0; q < W; ++q) v[k][q] = __ldcg(reinterpret_cast<const uint4*>(a.base[q] + off));
+          for (int q = 0; q < W; ++q) v[k][q] = __ldcg(reinterpret_cast<const uint4*>(a.base[q] + off));
+        } else {  // bitmaps pushed by the peers' compress kernels: all local
+#pragma unroll
+          for (int q = 0; q < W; ++q) {
+            const int64_t off = q == me ? a.off_bitmap[cur] + (i - t4) * 16
+                                        : a.off_inbox[cur] + (int64_t)q * a.words * 4 + (i - t4) * 16;
+            v[k][q] = __ldcg(reinterpret_cast<const uint4*>(a.base[me] + off));
+          }
+        }
       }
     }
 #pragma unroll

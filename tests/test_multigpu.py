@@ -29,6 +29,8 @@ VARIANTS = {
     "csig": {"S2_P2P_COMPRESS_SIGNAL": "1"},   # compress kernels signal completion to the peers
     "pipe": {"S2_P2P_PIPE": "1", "S2_P2P_ONESHOT_MAXW": "1"},  # pipelined two-shot, per-peer waits
     "blocks": {"S2_CHECK_NUM_BLOCKS": "62500"},  # block bitmap (b < d, 32 elements per block)
+    "push": {"S2_P2P_BITMAP_PUSH_MAXW": "8"},  # compress stores its bitmap into the peers' inboxes
+    "push_graph": {"S2_P2P_BITMAP_PUSH_MAXW": "8", "S2_CHECK_GRAPH": "1"},
 }
 
 

@@ -46,22 +46,18 @@ if os.environ.get("S2_CHECK_GRAPH") == "1":  # replay captured CUDA graphs inste
     out_static = torch.empty(a.dim, device="cuda")
     graphed = GraphedReduce(red, g_static, out_static)
 report = {"world": world, "dim": a.dim, "graph": graphed is not None}
-for kind in ("int", "normal"):
-    grads = [o.synthetic_gradient(a.dim, a.alpha, r, kind=kind) for r in range(world)]
-    for rep in range(2):  # twice: exercises the ping-pong tables
-        if graphed is None:
-            out = red.reduce(torch.from_numpy(grads[rank]).cuda()).cpu().numpy()
-        else:
-            g_static.copy_(torch.from_numpy(grads[rank]))
-            out = graphed().cpu().numpy()
+# three inputs with different non-zero positions (base seeds), each reduced twice, every
+# output checked: a stale bitmap or table from the previous call of the same ping-pong
+# parity would show up as a parity failure
+CASES = (("int", "int", 1234), ("normal", "normal", 1234), ("normal_b", "normal", 4321))
+for name, kind, base in CASES:
+    grads = [o.synthetic_gradient(a.dim, a.alpha, r, kind=kind, base_seed=base) for r in range(world)]
     ps = [o.compress(g, o.nonzero_flags(g, nb), a.rows, a.cols, 0) for g in grads]
     m = o.merge(ps)
     ref = o.decompress(m)
-    if kind == "int":
-        ok = bool(np.array_equal(out, ref.astype(np.float32)))
-        err = float(np.abs(out - ref).max())
-    else:
-        union = o.selected_indices(m.flags, a.dim)
+    union = o.selected_indices(m.flags, a.dim)
+    mmax = None
+    if kind != "int":
         mass = np.zeros((a.rows, a.cols))
         for g, p in zip(grads, ps):
             idx = o.selected_indices(p.flags, a.dim)
@@ -70,18 +66,30 @@ for kind in ("int", "normal"):
         mmax = np.zeros(union.size)
         for j, s in enumerate(o.row_seeds(0, a.rows)):
             mmax = np.maximum(mmax, mass[j, o.hash_buckets(s, union, a.cols)])
-        e = np.abs(out[union].astype(np.float64) - ref[union])
-        outside = np.ones(a.dim, bool)
-        outside[union] = False
-        ok = bool((e <= 1e-5 * mmax / world + 1e-30).all() and not out[outside].any())
-        err = float((e / np.maximum(mmax / world, 1e-30)).max())
-    h = hashlib.sha256(out.tobytes()).hexdigest()
+    outside = np.ones(a.dim, bool)
+    outside[union] = False
+    oks_rep, errs, hashes = [], [], []
+    for rep in range(2):  # twice: both ping-pong buffers
+        if graphed is None:
+            out = red.reduce(torch.from_numpy(grads[rank]).cuda()).cpu().numpy()
+        else:
+            g_static.copy_(torch.from_numpy(grads[rank]))
+            out = graphed().cpu().numpy()
+        if kind == "int":
+            oks_rep.append(bool(np.array_equal(out, ref.astype(np.float32))))
+            errs.append(float(np.abs(out - ref).max()))
+        else:
+            e = np.abs(out[union].astype(np.float64) - ref[union])
+            oks_rep.append(bool((e <= 1e-5 * mmax / world + 1e-30).all() and not out[outside].any()))
+            errs.append(float((e / np.maximum(mmax / world, 1e-30)).max()))
+        hashes.append(hashlib.sha256(out.tobytes()).hexdigest())
     hs = [None] * world
-    dist.all_gather_object(hs, h)
-    report[kind] = {"parity": ok, "max_err": err, "replicated": len(set(hs)) == 1,
+    dist.all_gather_object(hs, hashes)
+    report[name] = {"parity": all(oks_rep), "max_err": max(errs),
+                    "replicated": all(len({h[k] for h in hs}) == 1 for k in range(2)),
                     "nnz_union": int(m.flags.sum())}
 oks = [None] * world
-dist.all_gather_object(oks, all(report[k]["parity"] and report[k]["replicated"] for k in ("int", "normal")))
+dist.all_gather_object(oks, all(report[c[0]]["parity"] and report[c[0]]["replicated"] for c in CASES))
 report["all_ranks_ok"] = all(oks)
 if rank == 0:
     print(json.dumps(report), flush=True)
