@@ -427,3 +427,36 @@ def test_split_compress_variant(s2):
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=root,
                        env=dict(os.environ, S2_COMPRESS_SPLIT="1", PYTHONPATH=root), timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_random_shapes_bit_exact(s2):
+    """Fuzz: random dims (ragged tiles and words), block counts, rows 1..16, non-power-of-two and
+    tiny widths, 64-bit seeds, W = 1..5 and densities, integer values (every cell sum < 2^24) —
+    bitmaps, merged tables and decodes bit-exact against the oracle through the functional API."""
+    rng = np.random.default_rng(2110)
+    for trial in range(40):
+        dim = int(rng.integers(1, 300_000))
+        nb = dim if rng.random() < 0.6 else int(rng.integers(1, dim + 1))
+        rows = int(rng.choice([1, 2, 3, 4, 5, 7, 8, 16]))
+        W = int(rng.integers(1, 6))
+        dens = float(rng.choice([0.0005, 0.01, 0.1, 0.5]))
+        nnz = max(1, int(dens * dim))
+        cols = max(1, int(rng.integers(max(1, W * nnz // 8000), max(2, W * nnz // 8000) + 5000)))
+        seed = int(rng.integers(0, 2**63))
+        grads = []
+        for w in range(W):
+            g = np.zeros(dim, np.float32)
+            pos = rng.choice(dim, min(nnz, dim), replace=False)
+            v = rng.integers(-1000, 1001, pos.size).astype(np.float32)
+            v[v == 0] = 1.0
+            g[pos] = v
+            grads.append(g)
+        ps = [s2.sparse_compress(cuda(g), None, rows, cols, seed, num_blocks=nb) for g in grads]
+        ops = [o.compress(g, o.nonzero_flags(g, nb), rows, cols, seed) for g in grads]
+        for p, q in zip(ps, ops):
+            assert np.array_equal(words_u32(p.mask.words)[: o.mask_words(q.flags).size], o.mask_words(q.flags)), trial
+            assert np.array_equal(host(p.table.table), q.table.astype(np.float32)), trial
+        m, om = s2.sparse_merge(ps), o.merge(ops)
+        assert np.array_equal(host(m.table.table), om.table.astype(np.float32)), trial
+        out = host(s2.sparse_decompress(m))
+        assert np.array_equal(out, o.decompress(om).astype(np.float32)), (trial, dim, nb, rows, cols, W)
