@@ -8,7 +8,9 @@ namespace s2 {
 
 // zt/zc: the NEXT reduce's sketch table and counters, zeroed here so that the next
 // compress needs no memset (plan ping-pong, s2_reduce); may be null.
-template <int R, bool BLOCKS>
+// PEERS: the union words are OR-ed from the W bitmaps in PeerMaps (opt-in exchange modes); a
+// separate instantiation so the default kernel does not carry that code (instruction cache).
+template <int R, bool BLOCKS, bool PEERS = false>
 __global__ void __launch_bounds__(kThreads)
 k_decode(const uint32_t* __restrict__ bitmap, int64_t dim, int64_t bs,
          const float* __restrict__ table, float workers, float inv_workers, int workers_pow2,
@@ -23,15 +25,13 @@ k_decode(const uint32_t* __restrict__ bitmap, int64_t dim, int64_t bs,
   const int wib = threadIdx.x >> 5;
   const int64_t ntiles = (dim + kTile - 1) / kTile;
   DecodeCtx c{bitmap, table, out, dim, bs, workers, inv_workers, workers_pow2};
-  if constexpr (!BLOCKS && (R == 3 || R == 5)) {  // opt-in peer-bitmap path: default row counts only
-    if (pm.n > 0) {
-      decode_range_peers<R>(c, pm, (int64_t)blockIdx.x * kWarps + wib, (int64_t)gridDim.x * kWarps, ntiles, hp,
-                            s_q[wib], s_v[wib]);
-      return;
-    }
-  }
-  decode_range<R, BLOCKS>(c, pm, (int64_t)blockIdx.x * kWarps + wib, (int64_t)gridDim.x * kWarps, ntiles, hp,
+  if constexpr (PEERS && !BLOCKS && (R == 3 || R == 5)) {  // 8-tile-ahead word prefetch
+    decode_range_peers<R>(c, pm, (int64_t)blockIdx.x * kWarps + wib, (int64_t)gridDim.x * kWarps, ntiles, hp,
                           s_q[wib], s_v[wib]);
+  } else {
+    decode_range<R, BLOCKS>(c, PEERS ? pm : PeerMaps{}, (int64_t)blockIdx.x * kWarps + wib,
+                            (int64_t)gridDim.x * kWarps, ntiles, hp, s_q[wib], s_v[wib]);
+  }
 }
 
 template <int R>
@@ -43,7 +43,10 @@ static void launch_decode_r(const Plan& p, const uint32_t* bitmap, const float* 
   const float inv = 1.0f / (float)workers;
   const int64_t zn4 = zt ? ((int64_t)p.hp.rows * p.hp.cols + 3) / 4 : 0;
   float4* z4 = reinterpret_cast<float4*>(zt);
-  if (p.block_size == 1)
+  if (p.block_size == 1 && pm.n > 0)
+    launch_ex(k_decode<R, false, true>, grid, kThreads, 0, st, bitmap, p.dim, (int64_t)1, table, (float)workers, inv,
+              pow2, out, z4, zn4, zc, p.hp, pm);
+  else if (p.block_size == 1)
     launch_ex(k_decode<R, false>, grid, kThreads, 0, st, bitmap, p.dim, (int64_t)1, table, (float)workers, inv, pow2,
               out, z4, zn4, zc, p.hp, pm);
   else
