@@ -288,11 +288,14 @@ def ours(args, cfg):
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    th0 = time.perf_counter()
     for i in range(args.steps):
         step(i)
+    host_us = (time.perf_counter() - th0) / args.steps * 1e6  # host enqueue cost per step
     e1.record(stream)
     barrier()
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    host_us = max_over_ranks(host_us)
 
     # per-phase durations: the same s2_reduce launches with the plan's timing events
     # (recorded on the launching stream between compress / aggregate / decode)
@@ -402,6 +405,7 @@ def ours(args, cfg):
                         "H2D/D2H of every step inside the timed region (CUDA events: first H2D start to "
                         "last D2H end; copies overlapped across steps on separate streams)"},
         "gpu_launches": args.steps * (3 if world > 1 else 2),
+        "host_enqueue_us_per_step": round(host_us, 2),
         "clocks": clk,
     }
     if dense is not None:
