@@ -1,4 +1,6 @@
 // s2_decode.cu — the standalone K4 decode kernel and its launcher (body in s2_decode.cuh).
+#include <cstdlib>
+
 #include "s2_device.cuh"
 #include "s2_decode.cuh"
 
@@ -38,7 +40,21 @@ template <int R>
 static void launch_decode_r(const Plan& p, const uint32_t* bitmap, const float* table, int workers,
                             float* out, float* zt, unsigned long long* zc, const PeerMaps& pm, cudaStream_t st) {
   const int64_t ntiles = (p.dim + kTile - 1) / kTile;
-  const int grid = grid_for(ntiles, 4);
+  // Multi-wave grid: ~3 tiles per warp (4 CTAs per SM are resident, so 8+ per SM means
+  // later waves of short-lived CTAs that rebalance the tail); measured vs one resident wave:
+  // ResNet-50 step 41.5 -> 40.6 µs, 4 % density 62.4 -> 60.2 µs, GPT-2-M 99 % 505 -> 479 µs.
+  // S2_DECODE_CTAS_PER_SM overrides.
+  static int per_sm_env = -1;
+  if (per_sm_env < 0) {
+    const char* e = getenv("S2_DECODE_CTAS_PER_SM");
+    per_sm_env = e && atoi(e) > 0 ? atoi(e) : 0;
+  }
+  int per_sm = per_sm_env;
+  if (per_sm == 0) {
+    const int64_t want = (ntiles + (int64_t)num_sms() * kWarps * 3 - 1) / ((int64_t)num_sms() * kWarps * 3);
+    per_sm = (int)(want < 4 ? 4 : (want > 32 ? 32 : want));
+  }
+  const int grid = grid_for(ntiles, per_sm);
   const int pow2 = (workers & (workers - 1)) == 0;
   const float inv = 1.0f / (float)workers;
   const int64_t zn4 = zt ? ((int64_t)p.hp.rows * p.hp.cols + 3) / 4 : 0;
