@@ -42,7 +42,8 @@ static void launch_decode_r(const Plan& p, const uint32_t* bitmap, const float* 
   const int64_t ntiles = (p.dim + kTile - 1) / kTile;
   // Multi-wave grid: ~3 tiles per warp (4 CTAs per SM are resident, so 8+ per SM means
   // later waves of short-lived CTAs that rebalance the tail); measured vs one resident wave:
-  // ResNet-50 step 41.5 -> 40.6 µs, 4 % density 62.4 -> 60.2 µs, GPT-2-M 99 % 505 -> 479 µs.
+  // ResNet-50 step 41.5 -> 40.6 µs, 4 % density 62.4 -> 60.2 µs, GPT-2-M 99 % 505 -> 471 µs
+  // (cap 48 per SM: 32 -> 48 gained 1.5 % at GPT-2-M 99 % and 3 % at the LSTM row bitmap).
   // S2_DECODE_CTAS_PER_SM overrides.
   static int per_sm_env = -1;
   if (per_sm_env < 0) {
@@ -52,7 +53,7 @@ static void launch_decode_r(const Plan& p, const uint32_t* bitmap, const float* 
   int per_sm = per_sm_env;
   if (per_sm == 0) {
     const int64_t want = (ntiles + (int64_t)num_sms() * kWarps * 3 - 1) / ((int64_t)num_sms() * kWarps * 3);
-    per_sm = (int)(want < 4 ? 4 : (want > 32 ? 32 : want));
+    per_sm = (int)(want < 4 ? 4 : (want > 48 ? 48 : want));
   }
   const int grid = grid_for(ntiles, per_sm);
   const int pow2 = (workers & (workers - 1)) == 0;
