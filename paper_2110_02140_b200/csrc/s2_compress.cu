@@ -644,6 +644,181 @@ k_insert_list(const uint2* __restrict__ list, float* __restrict__ table, unsigne
 
 // =================================================================== launchers
 
+// ------------------------------------- compress, warp-specialised variant (S2_COMPRESS_LOAD=5)
+//
+// One producer warp streams the CTA's tiles (t = blockIdx.x + j * gridDim.x) with cp.async.bulk
+// (one elected lane, completion on a per-stage "full" mbarrier) into kWsDepth 4 KB stages per
+// consumer warp; consumer warp c takes jobs j = c, c + C, ... (its own sub-ring, so a stage's
+// phases are always waited in order by one warp), reads its 8 float4 per lane from the stage,
+// runs the same scan / bitmap / queue / hash body as k_compress and releases the stage on its
+// "empty" mbarrier once the values are queued.  Up to C x kWsDepth tiles per CTA in flight, no
+// prefetch registers.
+constexpr int kWsConsumers = 8;
+constexpr int kWsDepth = 2;
+constexpr int kWsStages = kWsConsumers * kWsDepth;
+constexpr int kWsThreads = (kWsConsumers + 1) * 32;
+constexpr int kWsSmem = kWsStages * kTile * 4 + kWsConsumers * (32 + kQFast) * 8 + 2 * kWsStages * 8;
+
+template <int R>
+__global__ void __launch_bounds__(kWsThreads, 2)
+k_compress_ws(const float* __restrict__ g, int64_t dim, uint32_t* __restrict__ bitmap, float* __restrict__ table,
+              unsigned long long* __restrict__ counters, const __grid_constant__ HashParams hp) {
+  constexpr int kCap = 32 + kQFast;
+  extern __shared__ __align__(128) unsigned char ws_smem[];
+  float4* stages = reinterpret_cast<float4*>(ws_smem);                                     // [S][256]
+  uint32_t* s_qi = reinterpret_cast<uint32_t*>(ws_smem + kWsStages * kTile * 4);          // [C][kCap]
+  float* s_qv = reinterpret_cast<float*>(s_qi + kWsConsumers * kCap);                      // [C][kCap]
+  uint64_t* full = reinterpret_cast<uint64_t*>(s_qv + kWsConsumers * kCap);                // [S]
+  uint64_t* empty = full + kWsStages;                                                      // [S]
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int64_t ntiles = (dim + kTile - 1) / kTile;
+  const int64_t nfull = dim / kTile;
+  const int64_t nelem_words = (dim + 31) / 32;
+  // tiles of this CTA: t_j = blockIdx.x + j * gridDim.x, j < njobs
+  const int64_t njobs = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kWsStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  griddep_wait();  // g may be written by the caller's previous kernel
+  griddep_launch_dependents();
+
+  if (warp == kWsConsumers) {  // producer
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      for (int64_t j = 0; j < njobs; ++j) {
+        const int64_t t = blockIdx.x + j * gridDim.x;
+        if (t >= nfull) break;  // the ragged last tile is loaded by its consumer
+        const int64_t k = j / kWsConsumers;  // the consumer's k-th job
+        const int s = (int)(j % kWsConsumers) * kWsDepth + (int)(k % kWsDepth);
+        if (k >= kWsDepth) mbar_wait(&empty[s], (uint32_t)(((k / kWsDepth) - 1) & 1));
+        tma_load_1d(stages + s * (kTile / 4), g + t * kTile, kTile * 4, &full[s], pol);
+      }
+    }
+    return;
+  }
+
+  // consumers
+  uint32_t* qi = s_qi + warp * kCap;
+  float* qv = s_qv + warp * kCap;
+  const int src_grp = 8 * (lane & 3);
+  const int src_sh = 4 * (lane >> 2);
+  int qn = 0;
+  unsigned long long nnz = 0;
+  uint32_t bad = 0;
+  for (int64_t j = warp; j < njobs; j += kWsConsumers) {
+    const int64_t t = blockIdx.x + j * gridDim.x;
+    const int64_t base = t * kTile;
+    const int64_t kj = j / kWsConsumers;
+    const int s = warp * kWsDepth + (int)(kj % kWsDepth);
+    const bool staged = t < nfull;
+    float4 v[8];
+    const float4* st = stages + s * (kTile / 4);
+    if (staged) {
+      mbar_wait(&full[s], (uint32_t)((kj / kWsDepth) & 1));
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = st[k * 32 + lane];
+    } else {
+      load_tile(v, g, t, dim, lane);
+    }
+    uint32_t m = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      m |= ((uint32_t)(v[k].x != 0.f) << (4 * k)) | ((uint32_t)(v[k].y != 0.f) << (4 * k + 1)) |
+           ((uint32_t)(v[k].z != 0.f) << (4 * k + 2)) | ((uint32_t)(v[k].w != 0.f) << (4 * k + 3));
+    }
+    const int cnt = __popc(m);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += n;
+    }
+    const int total = __shfl_sync(kFull, incl, 31);
+    uint32_t word = 0;
+    if (total) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t mq = __shfl_sync(kFull, m, src_grp + q);
+        word |= ((mq >> src_sh) & 0xFu) << (4 * q);
+      }
+      nnz += (unsigned)total;
+      if (staged && qn + total <= kCap) {
+        // walk the set bits, values straight from the stage (bit 4k+c <-> offset 128k + 4*lane + c)
+        const float* sf = reinterpret_cast<const float*>(st);
+        int pos = qn + incl - cnt;
+        for (uint32_t mm = m; mm; mm &= mm - 1u) {
+          const int b = __ffs(mm) - 1;
+          const uint32_t off = 128u * (uint32_t)(b >> 2) + 4u * lane + (uint32_t)(b & 3);
+          qi[pos] = (uint32_t)base + off;
+          qv[pos] = sf[off];
+          ++pos;
+        }
+        qn += total;
+        flush_full<R>(qi, qv, qn, lane, table, hp, bad);
+      } else {
+      const uint32_t lt = lanemask_lt();
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {  // chunk by chunk (<= 128 per chunk), flushing full batches
+        const uint32_t nib = (m >> (4 * k)) & 0xFu;
+        const uint32_t b0 = __ballot_sync(kFull, nib & 1u);
+        const uint32_t b1 = __ballot_sync(kFull, nib & 2u);
+        const uint32_t b2 = __ballot_sync(kFull, nib & 4u);
+        const uint32_t b3 = __ballot_sync(kFull, nib & 8u);
+        const int tot = __popc(b0) + __popc(b1) + __popc(b2) + __popc(b3);
+        if (tot == 0) continue;
+        int pos = qn + __popc(b0 & lt) + __popc(b1 & lt) + __popc(b2 & lt) + __popc(b3 & lt);
+        const uint32_t e = (uint32_t)(base + k * 128 + lane * 4);
+        if (nib & 1u) { qi[pos] = e + 0; qv[pos] = v[k].x; ++pos; }
+        if (nib & 2u) { qi[pos] = e + 1; qv[pos] = v[k].y; ++pos; }
+        if (nib & 4u) { qi[pos] = e + 2; qv[pos] = v[k].z; ++pos; }
+        if (nib & 8u) { qi[pos] = e + 3; qv[pos] = v[k].w; ++pos; }
+        qn += tot;
+        if (qn >= 32) flush_full<R>(qi, qv, qn, lane, table, hp, bad);
+      }
+      }
+    }
+    __syncwarp();
+    if (staged && lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
+    const int64_t wi = t * 32 + lane;
+    if (wi < nelem_words) bitmap[wi] = word;
+  }
+  __syncwarp();
+  if (lane < qn) {
+    const float v = qv[lane];
+    bad |= nonfinite(v);
+    insert_one<R>(qi[lane], v, table, hp);
+  }
+  bad = __any_sync(kFull, bad);
+  if (lane == 0) {
+    if (nnz) {
+      atomicAdd(counters + S2_CNT_NNZ, nnz);
+      atomicAdd(counters + S2_CNT_SELECTED, nnz);
+    }
+    if (bad) atomicOr(counters + S2_CNT_NONFINITE, 1ull);
+  }
+}
+
+template <int R>
+static void launch_compress_ws(const Plan& p, const float* g, uint32_t* bitmap, float* table,
+                               unsigned long long* counters, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_compress_ws<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, kWsSmem);
+    attr = true;
+  }
+  const int64_t ntiles = (p.dim + kTile - 1) / kTile;
+  int64_t grid = (int64_t)num_sms() * 2;
+  if (grid > ntiles) grid = ntiles;
+  launch_ex(k_compress_ws<R>, (int)(grid < 1 ? 1 : grid), kWsThreads, kWsSmem, st, g, p.dim, bitmap, table, counters,
+            p.hp);
+}
+
 // S2_COMPRESS_LOAD: 0 register prefetch (default: fastest measured, profiles/r01_*) |
 //                   1 TMA prefetch, coalesced layout | 2 TMA-staged 2-stage ring, swizzled
 static int compress_variant() {
@@ -651,7 +826,7 @@ static int compress_variant() {
   if (v < 0) {
     const char* e = getenv("S2_COMPRESS_LOAD");
     v = e ? atoi(e) : 0;
-    if (v < 0 || v > 3) v = 0;
+    if (v < 0 || v > 5 || v == 4) v = 0;
   }
   return v;
 }
@@ -719,6 +894,8 @@ static void launch_compress_r(const Plan& p, const float* g, uint32_t* bitmap, f
   if constexpr (R == 3) {
     if (v == 3) return launch_compress_rm<R, 3>(p, g, bitmap, table, counters, mode, st, sig, push);
     if (v == 1) return launch_compress_rm<R, 1>(p, g, bitmap, table, counters, mode, st, sig, push);
+    if (v == 5 && mode != S2_MASK_GIVEN && p.block_size == 1)
+      return launch_compress_ws<R>(p, g, bitmap, table, counters, st);
     if (v == 2) {
       if (mode == S2_MASK_GIVEN) return launch_compress_tma<R, 2>(p, g, bitmap, table, counters, st);
       if (p.block_size == 1) return launch_compress_tma<R, 0>(p, g, bitmap, table, counters, st);
