@@ -460,3 +460,20 @@ def test_random_shapes_bit_exact(s2):
         assert np.array_equal(host(m.table.table), om.table.astype(np.float32)), trial
         out = host(s2.sparse_decompress(m))
         assert np.array_equal(out, o.decompress(om).astype(np.float32)), (trial, dim, nb, rows, cols, W)
+
+
+@pytest.mark.parametrize("load", ["1", "2", "3", "5"])
+def test_compress_load_variants(load):
+    """The opt-in compress load schemes (S2_COMPRESS_LOAD, read once per process: run in a child
+    pytest) pass the golden, fuzz and full-size ResNet parity tests like the default kernel."""
+    import subprocess
+    import sys
+
+    if os.environ.get("S2_VARIANT_CHILD"):
+        pytest.skip("inside a variant child run")
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, S2_COMPRESS_LOAD=load, S2_VARIANT_CHILD="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", os.path.join(here, "test_gpu_parity.py"),
+                        "-k", "golden_case or random_shapes or full_size"], capture_output=True, text=True,
+                       timeout=600, env=env, cwd=os.path.dirname(here))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]

@@ -31,6 +31,7 @@ VARIANTS = {
     "blocks": {"S2_CHECK_NUM_BLOCKS": "62500"},  # block bitmap (b < d, 32 elements per block)
     "push": {"S2_P2P_BITMAP_PUSH_MAXW": "8"},  # compress stores its bitmap into the peers' inboxes
     "push_graph": {"S2_P2P_BITMAP_PUSH_MAXW": "8", "S2_CHECK_GRAPH": "1"},
+    "coop": {"S2_P2P_COOP": "1", "S2_P2P_GRID": "148"},  # cooperative launch, one CTA per SM
 }
 
 
