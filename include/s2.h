@@ -48,6 +48,10 @@ extern "C" {
 #define S2_CNT_SELECTED 2  /* coordinates inside set blocks (alpha * dim)      */
 #define S2_NUM_COUNTERS 4
 
+/* status word written by every s2_reduce when set (s2_plan_set_status) */
+#define S2_STATUS_NONFINITE 1u /* this rank's gradient held NaN/Inf (core.py:157-158)            */
+#define S2_STATUS_EXCHANGE 2u  /* a cross-rank barrier timed out: the output was set to NaN      */
+
 /* mask modes for s2_compress */
 #define S2_MASK_NONZERO 0 /* build the bitmap: flag = block holds a non-zero */
 #define S2_MASK_GIVEN 1   /* bitmap is an input (e.g. block_topk, sparse.py:70-80)         */
@@ -124,27 +128,36 @@ int64_t s2_compact_scratch_bytes(const s2_plan* plan);
 int s2_compact(const s2_plan* plan, const uint32_t* bitmap, const float* g, int64_t* idx_out,
                float* val_out, int64_t* count, void* scratch, void* stream);
 
-/* ---- distributed reduce over NCCL / NVLink (replaces the in-process
+/* ---- distributed reduce over NVLink peer memory / NCCL (replaces the in-process
  *      sparse_merge list fold, sparse.py:174-196) -------------------------- */
 int s2_nccl_unique_id(void* out /* 128 bytes */);
+/* optional, before s2_comm_init*: exchange-kernel CTAs per rank (0 = default: one per SM, or
+ * one per two SMs for exchanges <= 8 MB) and the cross-rank barrier timeout in seconds
+ * (<= 0: S2_P2P_TIMEOUT_S or 300 s).  After a timeout the plan's outputs are NaN and
+ * S2_STATUS_EXCHANGE is reported — never a silently incomplete average. */
+int s2_comm_set_options(s2_plan* plan, int exchange_grid, double timeout_s);
 int s2_comm_init(s2_plan* plan, int world, int rank, const void* unique_id);
-/* comm modes: IPC = plan allocates a CUDA-IPC arena (default); NCCL = NCCL collectives only;
- * EXTERNAL = caller provides symmetric memory through s2_comm_attach (e.g. torch
- * symmetric memory with an NVLS multicast address) */
+/* comm modes: IPC = the plan allocates its exchange arena, CUDA-IPC handles travel through
+ * one NCCL all-gather (default); NCCL = NCCL all-reduce + all-gather + OR kernel;
+ * EXTERNAL = no NCCL at all: the caller provides every rank's arena through s2_comm_attach
+ * (torch symmetric memory, or W plans driven from one process — the single-GPU multi-rank
+ * harness) and checks s2_plan_digest across ranks itself.  unique_id may be NULL. */
 #define S2_COMM_IPC 0
 #define S2_COMM_NCCL 1
 #define S2_COMM_EXTERNAL 2
 int s2_comm_init_mode(s2_plan* plan, int world, int rank, const void* unique_id, int mode);
 /* bytes of the per-rank exchange arena for `world` ranks (same on every rank) */
 int64_t s2_p2p_arena_bytes(s2_plan* plan, int world);
-/* attach symmetric memory: bases[q] = rank q's arena mapped in this process, mc_base =
- * multicast (NVLS) address of the arena or 0.  With mc_base != 0 the sketch SUM and bitmap
- * OR are reduced inside the NVSwitch (multimem.ld_reduce + multimem.st). */
-int s2_comm_attach(s2_plan* plan, const uint64_t* bases, int world, uint64_t mc_base);
-/* one-time agreement on (dim, num_blocks, rows, cols, seed) across ranks —
- * the distributed compat_key check (sparse.py:105-109, :179-187) */
+/* EXTERNAL mode: bases[q] = rank q's arena (s2_p2p_arena_bytes bytes, 256-B aligned) as
+ * addressable from this process/device; zeroes this rank's arena (stream 0).  Every rank must
+ * attach before any rank reduces. */
+int s2_comm_attach(s2_plan* plan, const uint64_t* bases, int world);
+/* compat_key digest of (dim, num_blocks, rows, cols, seed, injective) (sparse.py:105-109) */
+uint64_t s2_plan_digest(const s2_plan* plan);
+/* one-time agreement on the digest across ranks over NCCL (IPC / NCCL modes; EXTERNAL: no-op,
+ * the caller compares s2_plan_digest) — the distributed compat_key check (sparse.py:179-187) */
 int s2_comm_check(s2_plan* plan, void* stream);
-/* sketch all-reduce (sum) in place + bitmap all-gather fused with OR into union */
+/* sketch all-reduce (sum) in place + bitmap all-gather fused with OR into union (NCCL) */
 int s2_aggregate(s2_plan* plan, float* table, const uint32_t* bitmap, uint32_t* union_out,
                  void* stream);
 /* the whole reduce: compress -> aggregate -> decode (÷ world) using plan-owned
@@ -153,12 +166,16 @@ int s2_aggregate(s2_plan* plan, float* table, const uint32_t* bitmap, uint32_t* 
  * counters alternate between consecutive calls (the decode of call i zeroes the
  * buffers of call i+1), so a CUDA graph must capture an even number of calls. */
 int s2_reduce(s2_plan* plan, const float* g, float* out, uint64_t* counters, void* stream);
+/* every later s2_reduce's decode writes its S2_STATUS_* bits (0 = healthy) into *status
+ * (device memory or mapped pinned host memory; NULL disables) — lets a caller check the
+ * previous step without synchronising */
+int s2_plan_set_status(s2_plan* plan, uint32_t* status);
 /* device pointer to the counters of the most recent s2_reduce(counters = NULL) */
 const uint64_t* s2_last_counters(const s2_plan* plan);
 /* optional: 4 caller-created cudaEvent_t that s2_reduce records before compress,
  * after compress, after aggregate and after decode (n = 0 disables) */
 int s2_plan_set_timing_events(s2_plan* plan, void* const* events, int n);
-/* != 0 if a peer-memory barrier gave up after 10 s (a rank died or diverged); syncs */
+/* != 0 if a peer-memory barrier timed out (a rank died or diverged); synchronises */
 int s2_p2p_error(const s2_plan* plan);
 /* debugging: globaltimer stamps [G][8] of the last peer-memory exchange (S2_P2P_TRACE=1) */
 int s2_p2p_trace(const s2_plan* plan, uint64_t* host, int64_t n);

@@ -44,6 +44,17 @@ def _grad(dim, alpha, rank, kind, base_seed=1234):
     elif kind == "int":
         vals = rng.integers(-1000, 1001, size=nnz).astype(np.float32)
         vals[vals == 0] = 1.0
+    elif kind == "subint":
+        # fp32 subnormals: integers in units of 2^-149 (every partial sum stays subnormal and exact)
+        k = rng.integers(-1000, 1001, size=nnz).astype(np.float64)
+        k[k == 0] = 1.0
+        vals = (k * 2.0 ** -149).astype(np.float32)
+    elif kind == "underflow":
+        # just above the normal range (+-[1, 1.5] x 2^-126): cells of opposite signs cancel into
+        # the subnormal range, which a flush-to-zero accumulation would lose
+        k = rng.integers(2 ** 23, 2 ** 23 + 2 ** 22, size=nnz).astype(np.float64)
+        k *= rng.integers(0, 2, size=nnz) * 2.0 - 1.0
+        vals = (k * 2.0 ** -149).astype(np.float32)
     else:
         raise ValueError(kind)
     g = np.zeros(dim, dtype=np.float32)
@@ -137,8 +148,16 @@ def case(core, sparse, name, dim, alpha, rows, cols, W, kind, num_blocks=None, s
         nbytes=payloads[0].serialized_nbytes(),
         wire_sha256=np.frombuffer(hashlib.sha256(payloads[0].to_bytes()).digest(), np.uint8),
         wire_head=np.frombuffer(payloads[0].to_bytes()[:53], np.uint8),
+        # CommCost of worker 0's payload and of the merged payload (sparse.py:244-285)
+        comm_bits=_comm(sparse.sparse_comm_bits(payloads[0])),
+        comm_bits_merged=_comm(sparse.sparse_comm_bits(m)),
     )
     np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **d)
+
+
+def _comm(c):
+    return np.array([c.payload_bits, c.dense_bits, c.coordinate_bits, c.value_bits, c.bitmap_bits, c.header_bits],
+                    dtype=np.int64)
 
 
 def main():
@@ -165,6 +184,9 @@ def main():
     case(core, sparse, "s2_edge37", 37, 0.0, 3, 5, 2, "normal",
          extra=[g_edge, np.zeros(37, np.float32)])
     case(core, sparse, "s2_d1", 1, 0.0, 3, 2, 1, "normal", extra=[np.array([-3.0], np.float32)])
+    # fp32 subnormal and underflowing values (the reference adds in float64, sketch.py:111)
+    case(core, sparse, "s2_subnormal_int", 30_011, 0.05, 3, 97, 3, "subint")
+    case(core, sparse, "s2_underflow", 20_000, 0.1, 3, 53, 2, "underflow")
     print("golden written to", os.path.abspath(OUT))
 
 

@@ -304,6 +304,16 @@ def decompress(payload: Payload, workers=None) -> np.ndarray:
     return out
 
 
+def comm_bits(payload: Payload) -> tuple:
+    """sparse_comm_bits (sparse.py:264-285): (payload, dense, coordinate, value, bitmap, header) bits;
+    the coordinate baseline is 32 bits + ceil(log2 dim) index bits per selected coordinate."""
+    nb = payload.flags.size
+    nnz = int(block_sizes(payload.dim, nb)[payload.flags].sum())
+    index_bits = max(1, (payload.dim - 1).bit_length())
+    return (8 * payload.serialized_nbytes(), 32 * payload.dim, nnz * (32 + index_bits),
+            32 * payload.rows * payload.cols, nb, 8 * (4 + 1 + 6 * 8))
+
+
 def reduce(grads, num_blocks, rows, cols, seed):
     """Whole-box reduce on W gradients with the non-zero mask rule (north-star path)."""
     ps = [compress(g, nonzero_flags(g, num_blocks), rows, cols, seed) for g in grads]

@@ -28,6 +28,11 @@ S2_CNT_SELECTED = 2
 S2_NUM_COUNTERS = 4
 S2_MASK_NONZERO = 0
 S2_MASK_GIVEN = 1
+S2_STATUS_NONFINITE = 1
+S2_STATUS_EXCHANGE = 2
+S2_COMM_IPC = 0
+S2_COMM_NCCL = 1
+S2_COMM_EXTERNAL = 2
 
 # every symbol include/s2.h declares: name -> (restype, argtypes)
 SIGNATURES = {
@@ -53,10 +58,13 @@ SIGNATURES = {
     "s2_block_topk": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
     "s2_compact": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "s2_nccl_unique_id": (c_int, [c_void_p]),
+    "s2_comm_set_options": (c_int, [c_void_p, c_int, ctypes.c_double]),
     "s2_comm_init": (c_int, [c_void_p, c_int, c_int, c_void_p]),
     "s2_comm_init_mode": (c_int, [c_void_p, c_int, c_int, c_void_p, c_int]),
     "s2_p2p_arena_bytes": (c_int64, [c_void_p, c_int]),
-    "s2_comm_attach": (c_int, [c_void_p, POINTER(c_uint64), c_int, c_uint64]),
+    "s2_comm_attach": (c_int, [c_void_p, POINTER(c_uint64), c_int]),
+    "s2_plan_digest": (c_uint64, [c_void_p]),
+    "s2_plan_set_status": (c_int, [c_void_p, c_void_p]),
     "s2_comm_check": (c_int, [c_void_p, c_void_p]),
     "s2_aggregate": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "s2_reduce": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),

@@ -32,18 +32,17 @@ struct s2_plan {
   uint32_t* unionmap = nullptr;
   uint32_t* gather = nullptr;  // world * words (all-gather landing buffer)
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // optional phase timing events
-  // NVLink peer-memory exchange (world > 1, default): one IPC-shared arena per rank
+  uint32_t* status = nullptr;  // S2_STATUS_* of every reduce (s2_plan_set_status)
+  // NVLink peer-memory exchange (world > 1, default): one arena per rank, mapped by every rank
   bool p2p = false;
   char* arena = nullptr;
   char* peer[s2::kMaxWorld] = {};
   s2::P2PArgs pa{};
   int p2p_grid = 0;
-  bool fused = false;  // W > 1: one k_xdecode launch replaces exchange + decode
-  int x_grid = 0;
   int comm_mode = 0;         // S2_COMM_IPC | S2_COMM_NCCL | S2_COMM_EXTERNAL
-  void* list = nullptr;      // split compress: (index, value) list, dim x 8 B (lazy)
-  int split = -1;            // -1: decide from S2_COMPRESS_SPLIT
-  bool arena_owned = false;  // cudaMalloc'd here (IPC) vs attached symmetric memory
+  bool arena_owned = false;  // cudaMalloc'd here (IPC) vs attached by the caller (EXTERNAL)
+  int opt_grid = 0;          // s2_comm_set_options
+  double opt_timeout_s = 0;
 };
 
 namespace {
@@ -116,7 +115,7 @@ cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 extern "C" {
 
 const char* s2_last_error(void) { return g_err.c_str(); }
-int s2_abi_version(void) { return 1; }
+int s2_abi_version(void) { return 2; }
 
 uint64_t s2_mix64(uint64_t x) { return s2::mix64(x); }
 
@@ -157,10 +156,10 @@ int s2_plan_create(int64_t dim, int64_t num_blocks, int rows, int64_t cols, uint
   HashParams hp;
   int rc = build_hash(seed, rows, cols, injective, &hp);
   if (rc) return rc;
-  if (injective && cols < dim) {
-    // HashMapping(injective) raises only when a selected index >= buckets (core.py:131-135);
-    // the Python layer performs that check, the kernels never index past cols.
-  }
+  // injective with cols < dim is legal: HashMapping(injective) raises only when an index it
+  // maps is >= buckets (core.py:131-135).  The Python layer raises that ValueError before any
+  // kernel runs; the kernels skip (insert) or read 0 for (query) such indices, so a direct
+  // C-ABI caller cannot write or read past the table.
   s2_plan* p = new s2_plan();
   p->p.dim = dim;
   p->p.num_blocks = num_blocks;
@@ -201,7 +200,6 @@ static void free_p2p(s2_plan* p) {
 
 void s2_plan_destroy(s2_plan* plan) {
   if (!plan) return;
-  cudaFree(plan->list);
   free_p2p(plan);
   if (plan->comm) ncclCommDestroy(plan->comm);
   free_scratch(plan);
@@ -212,21 +210,6 @@ int64_t s2_plan_bitmap_words(const s2_plan* plan) { return plan ? plan->p.words 
 int64_t s2_plan_block_size(const s2_plan* plan) { return plan ? plan->p.block_size : -1; }
 int s2_plan_world(const s2_plan* plan) { return plan ? plan->world : -1; }
 
-static void* split_list(const s2_plan* cplan) {
-  s2_plan* plan = const_cast<s2_plan*>(cplan);  // lazily allocated scratch, not observable state
-  if (plan->split < 0) {
-    const char* e = getenv("S2_COMPRESS_SPLIT");
-    plan->split = e ? atoi(e) : 0;  // opt-in: measured slower than the fused kernel
-  }
-  if (!plan->split || plan->p.block_size != 1) return nullptr;
-  if (!plan->list && cudaMalloc(&plan->list, sizeof(uint64_t) * (size_t)plan->p.dim) != cudaSuccess) {
-    cudaGetLastError();
-    plan->split = 0;
-    return nullptr;
-  }
-  return plan->list;
-}
-
 int s2_compress(const s2_plan* plan, const float* g, uint32_t* bitmap, float* table, int mask_mode,
                 uint64_t* counters, void* stream) {
   if (!plan || !g || !bitmap || !table || !counters) return fail(S2_EINVAL, "NULL argument to s2_compress");
@@ -234,7 +217,7 @@ int s2_compress(const s2_plan* plan, const float* g, uint32_t* bitmap, float* ta
     return fail(S2_EINVAL, "unknown mask mode %d", mask_mode);
   if (reinterpret_cast<uintptr_t>(g) & 15) return fail(S2_EINVAL, "gradient must be 16-byte aligned");
   S2_CUDA(s2::launch_compress(plan->p, g, bitmap, table, reinterpret_cast<unsigned long long*>(counters),
-                              mask_mode, as_stream(stream), false, split_list(plan)),
+                              mask_mode, as_stream(stream), false),
           "s2_compress");
   return S2_OK;
 }
@@ -339,11 +322,9 @@ static int ensure_scratch(s2_plan* p) {
 
 static int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
-// One cudaMalloc arena per rank, exported with CUDA IPC and mapped by every peer:
-//   tables[2] | bitmaps[2] | unions[2] | flags_a[W*G] | flags_b[W*G] | epochs[G]
-// The handles travel through one ncclAllGather.
 // Arena layout (identical on every rank):
-//   tables[2] | bitmaps[2] | unions[2] | flags_a[W*G] | flags_b[W*G] | epochs[8G] | error | lsync | tsum[2]?
+//   tables[2] | bitmaps[2] | unions[2] | flags_a[W*8G] | flags_b[W*8G] | epochs[8G] | error | tsum[2]?
+// (flag and epoch slots for exchange grids of up to 8 CTAs per SM)
 static int64_t layout_p2p(s2_plan* plan, int W, int G) {
   const int64_t cells = round_up((int64_t)plan->p.hp.rows * plan->p.hp.cols, 4 * W);
   const int64_t words = round_up(plan->p.words, 4 * W);
@@ -357,45 +338,18 @@ static int64_t layout_p2p(s2_plan* plan, int W, int G) {
   for (int k = 0; k < 2; ++k) a.off_table[k] = take(cells * 4);
   for (int k = 0; k < 2; ++k) a.off_bitmap[k] = take(words * 4);
   for (int k = 0; k < 2; ++k) a.off_union[k] = take(words * 4);
-  a.off_flags_a = take((int64_t)W * 8 * G * 4);  // exchange grids up to 8 CTAs/SM (S2_P2P_GRID)
+  a.off_flags_a = take((int64_t)W * 8 * G * 4);
   a.off_flags_b = take((int64_t)W * 8 * G * 4);
-  a.off_epoch = take((int64_t)8 * G * 4);  // per-CTA epochs (fused grid <= 8 CTAs/SM)
+  a.off_epoch = take((int64_t)8 * G * 4);
   a.off_error = take(256);
-  a.off_lsync = take(256);
-  a.off_flags_c = take(256);  // [rank] = that rank's last compress epoch (signal_done)
-  a.off_cdone = take(256);    // this rank's compress CTA-done counter
-  a.off_cepoch = take(256);   // this rank's compress epoch
   const char* os_env = getenv("S2_P2P_ONESHOT_MAXW");
   const int oneshot_maxw = os_env ? atoi(os_env) : 2;
   a.oneshot = (W <= oneshot_maxw && W <= 4) ? 1 : 0;
-  // optional: the decode ORs the W bitmaps straight from peer memory and the exchange moves only
-  // the table (off by default: the per-tile NVLink latency stalls the decode)
-  const char* bd_env = getenv("S2_P2P_BITMAP_IN_DECODE_MAXW");
-  const int bd_maxw = bd_env ? atoi(bd_env) : 0;
-  a.table_only = (W <= bd_maxw && plan->p.block_size == 1 && (plan->p.hp.rows == 3 || plan->p.hp.rows == 5)) ? 1 : 0;
-  // optional: each compress also stores its bitmap words into every peer's inbox (remote NVLink
-  // stores hidden under the gradient stream), the exchange moves only the table and the decode
-  // ORs the W bitmaps from LOCAL memory
-  const char* bp_env = getenv("S2_P2P_BITMAP_PUSH_MAXW");
-  const int bp_maxw = bp_env ? atoi(bp_env) : 0;
-  a.push = (!a.table_only && W <= bp_maxw && plan->p.block_size == 1) ? 1 : 0;
-  for (int k = 0; k < 2; ++k) a.off_inbox[k] = a.push ? take((int64_t)W * words * 4) : -1;
-  // one-shot: the exchange ORs the pushed (local) bitmaps into the union itself;
-  // two-shot: the exchange moves only the table and the decode ORs the local copies
-  if (a.push && !a.oneshot) a.table_only = 1;
   for (int k = 0; k < 2; ++k) a.off_tsum[k] = a.oneshot ? take(cells * 4) : a.off_table[k];
   a.cells = cells;
   a.words = words;
   a.world = W;
   a.rank = plan->rank;
-  a.mc = nullptr;
-  a.nvls = 0;
-  const char* hv = getenv("S2_P2P_HIER");
-  a.hier = hv ? atoi(hv) : 0;
-  const char* cs = getenv("S2_P2P_COMPRESS_SIGNAL");
-  a.csig = cs ? atoi(cs) : 0;
-  const char* pp = getenv("S2_P2P_PIPE");
-  a.pipe = pp ? atoi(pp) : 0;
   return off;
 }
 
@@ -406,30 +360,29 @@ static int sm_count(int* G) {
   return S2_OK;
 }
 
-// base pointers known: plan tables into the arena, counters, trace, fused-kernel grid
+// base pointers known: plan tables into the arena, counters, trace, grid, timeout
 static int finish_p2p(s2_plan* plan, int G) {
   s2::P2PArgs& a = plan->pa;
-  const int W = plan->world;
   // exchange-kernel CTAs: one per SM, or one per two SMs when the exchanged table + bitmap
   // is small (<= 8 MB: fewer cross-rank flag pairs, measured ~1 µs per step faster at the
   // ResNet-50 config for W = 2 and 4; slower for the 12-56 MB exchanges)
   const int64_t xbytes = 4 * (a.cells + a.words);
-  plan->p2p_grid = (!a.nvls && xbytes <= (8ll << 20) && G >= 2) ? G / 2 : G;
-  const char* ge = getenv("S2_P2P_GRID");  // override
+  plan->p2p_grid = (xbytes <= (8ll << 20) && G >= 2) ? G / 2 : G;
+  const char* ge = getenv("S2_P2P_GRID");  // override (A/B runs)
   if (ge && atoi(ge) > 0 && atoi(ge) <= 8 * G) plan->p2p_grid = atoi(ge);
+  if (plan->opt_grid > 0) plan->p2p_grid = plan->opt_grid;
+  double tmo = plan->opt_timeout_s;
+  if (tmo <= 0) {
+    const char* te = getenv("S2_P2P_TIMEOUT_S");
+    tmo = te && atof(te) > 0 ? atof(te) : 300.0;
+  }
+  a.timeout_ns = (unsigned long long)(tmo * 1e9);
   plan->p2p = true;
   a.trace = nullptr;
   const char* tr = getenv("S2_P2P_TRACE");
   if (tr && atoi(tr)) {
     S2_CUDA(cudaMalloc(&a.trace, sizeof(unsigned long long) * 64 * G), "cudaMalloc(trace)");
     S2_CUDA(cudaMemset(a.trace, 0, sizeof(unsigned long long) * 64 * G), "cudaMemset(trace)");
-  }
-  plan->fused = false;
-  const char* fz = getenv("S2_FUSED");
-  if (fz && atoi(fz) != 0 && plan->p.block_size == 1 && !a.nvls && !a.push) {  // opt-in
-    cudaError_t e = s2::xdecode_grid(plan->p.hp, W, a.oneshot, &plan->x_grid);
-    if (e == cudaSuccess && plan->x_grid > 0) plan->fused = true;
-    else cudaGetLastError();
   }
   for (int k = 0; k < 2; ++k) {
     plan->tables[k] = reinterpret_cast<float*>(plan->arena + a.off_table[k]);
@@ -447,6 +400,7 @@ static int setup_p2p(s2_plan* plan) {
   int G = 0;
   int rc = sm_count(&G);
   if (rc) return rc;
+  if (plan->opt_grid > 8 * G) return fail(S2_EINVAL, "exchange grid must be <= %d", 8 * G);
   const int64_t off = layout_p2p(plan, W, G);
   s2::P2PArgs& a = plan->pa;
   S2_CUDA(cudaMalloc(&plan->arena, off), "cudaMalloc(arena)");
@@ -492,6 +446,15 @@ static int setup_p2p(s2_plan* plan) {
   return finish_p2p(plan, G);
 }
 
+int s2_comm_set_options(s2_plan* plan, int exchange_grid, double timeout_s) {
+  if (!plan) return fail(S2_EINVAL, "NULL plan");
+  if (plan->p2p || plan->comm) return fail(S2_EINVAL, "s2_comm_set_options must precede s2_comm_init");
+  if (exchange_grid < 0) return fail(S2_EINVAL, "exchange grid must be >= 0, got %d", exchange_grid);
+  plan->opt_grid = exchange_grid;
+  plan->opt_timeout_s = timeout_s;
+  return S2_OK;
+}
+
 int s2_comm_init_mode(s2_plan* plan, int world, int rank, const void* unique_id, int mode) {
   if (!plan) return fail(S2_EINVAL, "NULL plan");
   if (mode < S2_COMM_IPC || mode > S2_COMM_EXTERNAL) return fail(S2_EINVAL, "unknown comm mode %d", mode);
@@ -504,34 +467,32 @@ int64_t s2_p2p_arena_bytes(s2_plan* plan, int world) {
   int G = 0;
   if (sm_count(&G)) return -1;
   const int saved = plan->world;
+  const s2::P2PArgs saved_pa = plan->pa;
   plan->world = world;
   const int64_t b = layout_p2p(plan, world, G);
   plan->world = saved;
+  plan->pa = saved_pa;
   return b;
 }
 
-int s2_comm_attach(s2_plan* plan, const uint64_t* bases, int world, uint64_t mc_base) {
+int s2_comm_attach(s2_plan* plan, const uint64_t* bases, int world) {
   if (!plan || !bases) return fail(S2_EINVAL, "NULL argument to s2_comm_attach");
   if (plan->world != world || world < 2) return fail(S2_EINVAL, "attach: world %d does not match the plan", world);
   if (plan->comm_mode != S2_COMM_EXTERNAL) return fail(S2_EINVAL, "attach needs s2_comm_init_mode(..., S2_COMM_EXTERNAL)");
+  if (plan->p2p) return fail(S2_EINVAL, "arenas already attached");
   int G = 0;
   int rc = sm_count(&G);
   if (rc) return rc;
+  if (plan->opt_grid > 8 * G) return fail(S2_EINVAL, "exchange grid must be <= %d", 8 * G);
   const int64_t bytes = layout_p2p(plan, world, G);
   s2::P2PArgs& a = plan->pa;
   for (int q = 0; q < world; ++q) {
+    if (bases[q] == 0 || (bases[q] & 255)) return fail(S2_EINVAL, "arena %d must be non-NULL and 256-byte aligned", q);
     plan->peer[q] = reinterpret_cast<char*>(bases[q]);
     a.base[q] = plan->peer[q];
   }
   plan->arena = plan->peer[plan->rank];
   plan->arena_owned = false;
-  a.mc = reinterpret_cast<char*>(mc_base);
-  const char* nv = getenv("S2_NVLS");
-  a.nvls = (mc_base != 0 && !(nv && atoi(nv) == 0)) ? 1 : 0;
-  if (a.nvls && a.push) {  // the in-switch exchange reduces the bitmaps itself
-    a.push = 0;
-    a.table_only = 0;
-  }
   S2_CUDA(cudaMemset(plan->arena, 0, bytes), "cudaMemset(arena)");
   return finish_p2p(plan, G);
 }
@@ -539,18 +500,21 @@ int s2_comm_attach(s2_plan* plan, const uint64_t* bases, int world, uint64_t mc_
 int s2_comm_init(s2_plan* plan, int world, int rank, const void* unique_id) {
   if (!plan) return fail(S2_EINVAL, "NULL plan");
   if (world < 1 || rank < 0 || rank >= world) return fail(S2_EINVAL, "bad world/rank %d/%d", world, rank);
-  if (plan->comm) return fail(S2_EINVAL, "communicator already initialised");
+  if (plan->comm || plan->p2p) return fail(S2_EINVAL, "communicator already initialised");
   free_scratch(plan);
   plan->world = world;
   plan->rank = rank;
   if (world > 1) {
+    if (world > s2::kMaxWorld && plan->comm_mode != S2_COMM_NCCL)
+      return fail(S2_EINVAL, "peer-memory exchange supports world <= %d", s2::kMaxWorld);
+    if (plan->comm_mode == S2_COMM_EXTERNAL) return S2_OK;  // no NCCL: arenas come from s2_comm_attach
+    if (!unique_id) return fail(S2_EINVAL, "NULL NCCL unique id");
     ncclUniqueId id;
     memcpy(&id, unique_id, sizeof id);
     S2_NCCL(ncclCommInitRank(&plan->comm, world, id, rank), "ncclCommInitRank");
     const char* agg = getenv("S2_AGG");
     const bool nccl_only = (agg && strcmp(agg, "nccl") == 0) || plan->comm_mode == S2_COMM_NCCL;
-    if (!nccl_only && plan->comm_mode != S2_COMM_EXTERNAL) {
-      if (world > s2::kMaxWorld) return fail(S2_EINVAL, "peer-memory exchange supports world <= %d", s2::kMaxWorld);
+    if (!nccl_only) {
       int rc = setup_p2p(plan);
       if (rc) return rc;
     }
@@ -558,14 +522,20 @@ int s2_comm_init(s2_plan* plan, int world, int rank, const void* unique_id) {
   return ensure_scratch(plan);
 }
 
-int s2_comm_check(s2_plan* plan, void* stream) {
-  if (!plan) return fail(S2_EINVAL, "NULL plan");
-  if (plan->world == 1) return S2_OK;
+uint64_t s2_plan_digest(const s2_plan* plan) {
+  if (!plan) return 0;
   const Plan& q = plan->p;
-  // compat_key digest: partition + sketch params (sparse.py:105-109)
+  // compat_key: partition + sketch params (sparse.py:105-109)
   const uint64_t parts[7] = {(uint64_t)q.dim, (uint64_t)q.num_blocks, (uint64_t)q.hp.rows,
                              (uint64_t)q.hp.cols, q.seed, (uint64_t)q.injective, 0x53325348ull};
-  const uint64_t mine = derive(parts, 7);
+  return derive(parts, 7);
+}
+
+int s2_comm_check(s2_plan* plan, void* stream) {
+  if (!plan) return fail(S2_EINVAL, "NULL plan");
+  if (plan->world == 1 || plan->comm_mode == S2_COMM_EXTERNAL) return S2_OK;  // EXTERNAL: caller compares
+  if (!plan->comm) return fail(S2_EINVAL, "s2_comm_check needs s2_comm_init");
+  const uint64_t mine = s2_plan_digest(plan);
   uint64_t* d = nullptr;
   S2_CUDA(cudaMalloc(&d, sizeof(uint64_t) * (plan->world + 1)), "cudaMalloc(check)");
   cudaStream_t st = as_stream(stream);
@@ -620,6 +590,8 @@ int s2_reduce(s2_plan* plan, const float* g, float* out, uint64_t* counters, voi
   if (!plan || !g || !out) return fail(S2_EINVAL, "NULL argument to s2_reduce");
   if (reinterpret_cast<uintptr_t>(g) & 15) return fail(S2_EINVAL, "gradient must be 16-byte aligned");
   if (reinterpret_cast<uintptr_t>(out) & 15) return fail(S2_EINVAL, "output must be 16-byte aligned");
+  if (plan->world > 1 && !plan->p2p && !plan->comm)
+    return fail(S2_EINVAL, "world > 1 needs s2_comm_init (and s2_comm_attach in EXTERNAL mode)");
   int rc = ensure_scratch(plan);
   if (rc) return rc;
   cudaStream_t st = as_stream(stream);
@@ -629,60 +601,18 @@ int s2_reduce(s2_plan* plan, const float* g, float* out, uint64_t* counters, voi
   // caller counters: zeroed by memset; plan counters: zeroed by the previous decode
   unsigned long long* cnt = counters ? reinterpret_cast<unsigned long long*>(counters) : plan->counters[cur];
   if (plan->ev[0]) cudaEventRecord(plan->ev[0], st);
-  s2::DoneSignal sig{};
-  const bool use_push = plan->world > 1 && plan->p2p && plan->pa.push && !plan->pa.nvls && !plan->fused;
-  const bool use_sig = plan->world > 1 && plan->p2p && plan->pa.csig && !plan->pa.nvls && !plan->fused && !use_push;
-  s2::BitmapPush push{};
-  if (use_push) {  // slot [rank] of every peer's inbox[cur]
-    const int64_t slot = plan->pa.off_inbox[cur] + (int64_t)plan->rank * plan->pa.words * 4;
-    for (int q = 0; q < plan->world; ++q)
-      if (q != plan->rank) push.dst[push.n++] = reinterpret_cast<uint32_t*>(plan->pa.base[q] + slot);
-    static int fence = -1;
-    if (fence < 0) {
-      const char* f = getenv("S2_P2P_PUSH_FENCE");
-      fence = f ? atoi(f) : 1;
-    }
-    push.fence = fence;
-  }
-  if (use_sig) {
-    sig.done = reinterpret_cast<unsigned int*>(plan->arena + plan->pa.off_cdone);
-    sig.epoch = reinterpret_cast<unsigned int*>(plan->arena + plan->pa.off_cepoch);
-    for (int q = 0; q < plan->world; ++q)
-      sig.peer_flags[q] = reinterpret_cast<uint32_t*>(plan->pa.base[q] + plan->pa.off_flags_c);
-    sig.world = plan->world;
-    sig.rank = plan->rank;
-  }
-  S2_CUDA(s2::launch_compress(plan->p, g, bitmap, table, cnt, S2_MASK_NONZERO, st, counters == nullptr,
-                              (use_sig || use_push) ? nullptr : split_list(plan), use_sig ? &sig : nullptr,
-                              use_push ? &push : nullptr),
+  S2_CUDA(s2::launch_compress(plan->p, g, bitmap, table, cnt, S2_MASK_NONZERO, st, counters == nullptr),
           "s2_reduce/compress");
   if (plan->ev[1]) cudaEventRecord(plan->ev[1], st);
   const uint32_t* un = bitmap;
-  if (plan->world > 1 && plan->p2p && plan->fused) {
-    plan->pa.cur = cur;
-    s2::DecodeCtx dc{};
-    dc.out = out;
-    dc.dim = plan->p.dim;
-    dc.bs = 1;
-    dc.workers = (float)plan->world;
-    dc.inv_workers = 1.0f / (float)plan->world;
-    dc.workers_pow2 = (plan->world & (plan->world - 1)) == 0;
-    if (plan->ev[1]) cudaEventRecord(plan->ev[1], st);
-    if (plan->ev[2]) cudaEventRecord(plan->ev[2], st);
-    S2_CUDA(s2::launch_xdecode(plan->pa, dc, plan->p.hp, plan->x_grid, plan->tables[nxt],
-                               ((int64_t)plan->p.hp.rows * plan->p.hp.cols + 3) / 4, plan->counters[nxt], st),
-            "s2_reduce/fused exchange+decode");
-    if (plan->ev[3]) cudaEventRecord(plan->ev[3], st);
-    plan->phase = nxt;
-    return S2_OK;
-  }
+  s2::DecodeHealth health{nullptr, cnt, plan->status};
   if (plan->world > 1) {
     if (plan->p2p) {
       plan->pa.cur = cur;
       S2_CUDA(s2::launch_p2p_aggregate(plan->pa, plan->p2p_grid, st), "s2_reduce/p2p aggregate");
       un = reinterpret_cast<const uint32_t*>(plan->arena + plan->pa.off_union[cur]);
-      if (!plan->pa.nvls)  // one-shot sums into tsum; two-shot and NVLS reduce into tables[cur] in place
-        table = reinterpret_cast<float*>(plan->arena + plan->pa.off_tsum[cur]);
+      table = reinterpret_cast<float*>(plan->arena + plan->pa.off_tsum[cur]);  // two-shot: tables[cur] in place
+      health.poison = reinterpret_cast<const uint32_t*>(plan->arena + plan->pa.off_error);
     } else {
       rc = s2_aggregate(plan, table, bitmap, plan->unionmap, stream);
       if (rc) return rc;
@@ -690,20 +620,16 @@ int s2_reduce(s2_plan* plan, const float* g, float* out, uint64_t* counters, voi
     }
   }
   if (plan->ev[2]) cudaEventRecord(plan->ev[2], st);
-  s2::PeerMaps pm{};
-  if (plan->p2p && plan->pa.table_only) {
-    pm.n = plan->world;
-    for (int q = 0; q < plan->world; ++q)
-      pm.p[q] = reinterpret_cast<const uint32_t*>(
-          q == plan->rank || !plan->pa.push
-              ? plan->pa.base[q] + plan->pa.off_bitmap[cur]                                    // peer memory (NVLink)
-              : plan->arena + plan->pa.off_inbox[cur] + (int64_t)q * plan->pa.words * 4);  // pushed copy, local
-  }
-  S2_CUDA(s2::launch_decode(plan->p, un, table, plan->world, out, st, plan->tables[nxt], plan->counters[nxt],
-                            pm.n ? &pm : nullptr),
+  S2_CUDA(s2::launch_decode(plan->p, un, table, plan->world, out, st, plan->tables[nxt], plan->counters[nxt], &health),
           "s2_reduce/decode");
   if (plan->ev[3]) cudaEventRecord(plan->ev[3], st);
   plan->phase = nxt;
+  return S2_OK;
+}
+
+int s2_plan_set_status(s2_plan* plan, uint32_t* status) {
+  if (!plan) return fail(S2_EINVAL, "NULL plan");
+  plan->status = status;
   return S2_OK;
 }
 

@@ -10,35 +10,43 @@ namespace s2 {
 
 // zt/zc: the NEXT reduce's sketch table and counters, zeroed here so that the next
 // compress needs no memset (plan ping-pong, s2_reduce); may be null.
-// PEERS: the union words are OR-ed from the W bitmaps in PeerMaps (opt-in exchange modes); a
-// separate instantiation so the default kernel does not carry that code (instruction cache).
-template <int R, bool BLOCKS, bool PEERS = false>
+// health (s2_reduce only): a set poison word (exchange timed out) replaces the whole output
+// with NaN; block 0 reports the step's status word.
+template <int R, bool BLOCKS>
 __global__ void __launch_bounds__(kThreads)
 k_decode(const uint32_t* __restrict__ bitmap, int64_t dim, int64_t bs,
          const float* __restrict__ table, float workers, float inv_workers, int workers_pow2,
          float* __restrict__ out, float4* __restrict__ zt, int64_t zt_n4,
          unsigned long long* __restrict__ zc, const __grid_constant__ HashParams hp,
-         const __grid_constant__ PeerMaps pm) {
+         const __grid_constant__ DecodeHealth health) {
   zero_next(zt, zt_n4, zc);
   griddep_wait();  // bitmap + table come from the compress / exchange kernel
   griddep_launch_dependents();
+  const uint32_t poisoned = health.poison != nullptr ? *reinterpret_cast<volatile const uint32_t*>(health.poison) : 0u;
+  if (health.status != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
+    uint32_t st = poisoned ? S2_STATUS_EXCHANGE : 0u;
+    if (health.counters != nullptr && health.counters[S2_CNT_NONFINITE] != 0ull) st |= S2_STATUS_NONFINITE;
+    *reinterpret_cast<volatile uint32_t*>(health.status) = st;
+  }
+  if (poisoned) {  // a peer never arrived: the sums are incomplete, mark every coordinate invalid
+    const float nan = __int_as_float(0x7FC00000);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < dim; i += (int64_t)gridDim.x * blockDim.x)
+      out[i] = nan;
+    return;
+  }
   __shared__ uint16_t s_q[kWarps][kTile];
   __shared__ __align__(16) float s_v[kWarps][kTile];
   const int wib = threadIdx.x >> 5;
   const int64_t ntiles = (dim + kTile - 1) / kTile;
   DecodeCtx c{bitmap, table, out, dim, bs, workers, inv_workers, workers_pow2};
-  if constexpr (PEERS && !BLOCKS && (R == 3 || R == 5)) {  // 8-tile-ahead word prefetch
-    decode_range_peers<R>(c, pm, (int64_t)blockIdx.x * kWarps + wib, (int64_t)gridDim.x * kWarps, ntiles, hp,
-                          s_q[wib], s_v[wib]);
-  } else {
-    decode_range<R, BLOCKS>(c, PEERS ? pm : PeerMaps{}, (int64_t)blockIdx.x * kWarps + wib,
-                            (int64_t)gridDim.x * kWarps, ntiles, hp, s_q[wib], s_v[wib]);
-  }
+  decode_range<R, BLOCKS>(c, (int64_t)blockIdx.x * kWarps + wib, (int64_t)gridDim.x * kWarps, ntiles, hp, s_q[wib],
+                          s_v[wib]);
 }
 
 template <int R>
-static void launch_decode_r(const Plan& p, const uint32_t* bitmap, const float* table, int workers,
-                            float* out, float* zt, unsigned long long* zc, const PeerMaps& pm, cudaStream_t st) {
+static cudaError_t launch_decode_r(const Plan& p, const uint32_t* bitmap, const float* table, int workers,
+                                   float* out, float* zt, unsigned long long* zc, const DecodeHealth& health,
+                                   cudaStream_t st) {
   const int64_t ntiles = (p.dim + kTile - 1) / kTile;
   // Multi-wave grid: ~3 tiles per warp (4 CTAs per SM are resident, so 8+ per SM means
   // later waves of short-lived CTAs that rebalance the tail); measured vs one resident wave:
@@ -60,34 +68,27 @@ static void launch_decode_r(const Plan& p, const uint32_t* bitmap, const float* 
   const float inv = 1.0f / (float)workers;
   const int64_t zn4 = zt ? ((int64_t)p.hp.rows * p.hp.cols + 3) / 4 : 0;
   float4* z4 = reinterpret_cast<float4*>(zt);
-  if (p.block_size == 1 && pm.n > 0)
-    launch_ex(k_decode<R, false, true>, grid, kThreads, 0, st, bitmap, p.dim, (int64_t)1, table, (float)workers, inv,
-              pow2, out, z4, zn4, zc, p.hp, pm);
-  else if (p.block_size == 1)
-    launch_ex(k_decode<R, false>, grid, kThreads, 0, st, bitmap, p.dim, (int64_t)1, table, (float)workers, inv, pow2,
-              out, z4, zn4, zc, p.hp, pm);
-  else
-    launch_ex(k_decode<R, true>, grid, kThreads, 0, st, bitmap, p.dim, p.block_size, table, (float)workers, inv,
-              pow2, out, z4, zn4, zc, p.hp, pm);
+  if (p.block_size == 1)
+    return launch_ex(k_decode<R, false>, grid, kThreads, 0, st, bitmap, p.dim, (int64_t)1, table, (float)workers,
+                     inv, pow2, out, z4, zn4, zc, p.hp, health);
+  return launch_ex(k_decode<R, true>, grid, kThreads, 0, st, bitmap, p.dim, p.block_size, table, (float)workers, inv,
+                   pow2, out, z4, zn4, zc, p.hp, health);
 }
 
 cudaError_t launch_decode(const Plan& p, const uint32_t* bitmap, const float* table, int workers,
                           float* out, cudaStream_t st, float* zero_table, unsigned long long* zero_counters,
-                          const PeerMaps* peers) {
-  l2_window() = L2Window{table, sizeof(float) * (size_t)p.hp.rows * p.hp.cols};
-  struct Reset {
-    ~Reset() { l2_window() = L2Window{}; }
-  } reset_window;
-  PeerMaps pm{};
-  if (peers != nullptr && p.block_size == 1) pm = *peers;
+                          const DecodeHealth* health) {
+  DecodeHealth h{};
+  if (health != nullptr) h = *health;
+  cudaError_t e;
   switch (p.hp.rows) {
 #define S2_CASE(r) \
-  case r: launch_decode_r<r>(p, bitmap, table, workers, out, zero_table, zero_counters, pm, st); break;
-    S2_CASE(1) S2_CASE(2) S2_CASE(3) S2_CASE(4) S2_CASE(5) S2_CASE(6) S2_CASE(7) S2_CASE(8)
-    S2_CASE(9) S2_CASE(10) S2_CASE(11) S2_CASE(12) S2_CASE(13) S2_CASE(14) S2_CASE(15) S2_CASE(16)
+  case r: e = launch_decode_r<r>(p, bitmap, table, workers, out, zero_table, zero_counters, h, st); break;
+    S2_CASE(1) S2_CASE(2) S2_CASE(3) S2_CASE(4) S2_CASE(5)
 #undef S2_CASE
-    default: return cudaErrorInvalidValue;
+    default: e = launch_decode_r<0>(p, bitmap, table, workers, out, zero_table, zero_counters, h, st); break;
   }
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

@@ -1,6 +1,5 @@
 // s2_decode.cuh — the K4 decode body (sparse_decompress, sparse.py:199-214 + CountSketchTable.query,
-// sketch.py:114-128), shared by the standalone decode kernel (s2_kernels.cu) and the fused
-// exchange+decode kernel (s2_p2p.cu).
+// sketch.py:114-128), used by k_decode (s2_decode.cu) and k_query_pairs (s2_kernels.cu).
 #pragma once
 
 #include "s2_common.cuh"
@@ -35,44 +34,61 @@ __device__ __forceinline__ float lower_median(float (&e)[R]) {
   }
 }
 
+// R > 0: compile-time row count.  R == 0: any hp.rows <= S2_MAX_ROWS — the missing rows are
+// +inf, which sort last, so element (rows-1)/2 of the sorted 16 is the lower median.
 template <int R>
 __device__ __forceinline__ float query_one(uint64_t i, const float* __restrict__ table,
                                            const HashParams& hp) {
+  constexpr int N = R > 0 ? R : S2_MAX_ROWS;
   const size_t cols = hp.cols;
-  float e[R];
+  float e[N];
   if (hp.mode == kInjective) {
+    // i >= cols is rejected on the host (core.py:133-134); the guard keeps reads in bounds
 #pragma unroll
-    for (int j = 0; j < R; ++j) e[j] = __ldg(table + j * cols + i);
+    for (int j = 0; j < N; ++j)
+      e[j] = (R == 0 && j >= hp.rows) ? __int_as_float(0x7F800000) : (i < cols ? __ldg(table + j * cols + i) : 0.f);
   } else {
     const uint64_t x = index_term(i);
 #pragma unroll
-    for (int j = 0; j < R; ++j) {
+    for (int j = 0; j < N; ++j) {
+      if (R == 0 && j >= hp.rows) {
+        e[j] = __int_as_float(0x7F800000);
+        continue;
+      }
       const uint64_t w = mix64(hp.seed[j] + x);
       const float t = __ldg(table + j * cols + bucket_of(w, hp));
       e[j] = (w >> 63) ? -t : t;
     }
   }
-  return lower_median<R>(e);
+  if constexpr (R > 0) {
+    return lower_median<R>(e);
+  } else {
+#pragma unroll
+    for (int p = 0; p < N; ++p) {
+#pragma unroll
+      for (int a = (p & 1); a + 1 < N; a += 2) {
+        const float lo = fminf(e[a], e[a + 1]);
+        const float hi = fmaxf(e[a], e[a + 1]);
+        e[a] = lo;
+        e[a + 1] = hi;
+      }
+    }
+    float m = e[0];
+#pragma unroll
+    for (int j = 1; j < N; ++j)
+      if (j == (hp.rows - 1) / 2) m = e[j];
+    return m;
+  }
 }
 
 template <bool BLOCKS>
-__device__ __forceinline__ uint32_t decode_word(const uint32_t* __restrict__ bitmap, const PeerMaps& pm, int64_t t,
-                                               int lane, int64_t dim, int64_t bs, int64_t nelem_words) {
+__device__ __forceinline__ uint32_t decode_word(const uint32_t* __restrict__ bitmap, int64_t t, int lane, int64_t dim,
+                                               int64_t bs, int64_t nelem_words) {
   const int64_t e0 = t * kDecTile + 32 * lane;
   uint32_t word = 0;
   if (!BLOCKS) {
     const int64_t wi = t * 32 + lane;
-    if (wi < nelem_words) {
-      if (pm.n == 0) {
-        word = __ldg(bitmap + wi);
-      } else {
-        // union of the W ranks' bitmaps read straight from peer memory (NVLink) — the
-        // exchange kernel then only has to move the sketch table (BlockMask.union, sparse.py:55-58)
-#pragma unroll
-        for (int q = 0; q < kMaxWorld; ++q)
-          if (q < pm.n) word |= __ldcg(pm.p[q] + wi);
-      }
-    }
+    if (wi < nelem_words) word = __ldg(bitmap + wi);
   } else {
     word = expand_blocks(bitmap, e0, dim, bs);
   }
@@ -81,7 +97,7 @@ __device__ __forceinline__ uint32_t decode_word(const uint32_t* __restrict__ bit
 }
 
 struct DecodeCtx {
-  const uint32_t* bitmap;  // union bitmap (ignored when PeerMaps n > 0)
+  const uint32_t* bitmap;  // union bitmap
   const float* table;      // summed sketch table
   float* out;
   int64_t dim, bs;
@@ -153,54 +169,16 @@ __device__ __forceinline__ void decode_tile(const DecodeCtx& c, int64_t base, ui
 // Decode warp tiles t0, t0+tstep, ... < tend (one warp); the bitmap word is prefetched one
 // tile ahead.
 template <int R, bool BLOCKS>
-__device__ __forceinline__ void decode_range(const DecodeCtx& c, const PeerMaps& pm, int64_t t0, int64_t tstep,
-                                             int64_t tend, const HashParams& hp, uint16_t* q, float* vals) {
+__device__ __forceinline__ void decode_range(const DecodeCtx& c, int64_t t0, int64_t tstep, int64_t tend,
+                                             const HashParams& hp, uint16_t* q, float* vals) {
   const int lane = threadIdx.x & 31;
   const int64_t nelem_words = (c.dim + 31) / 32;
   int64_t t = t0;
-  uint32_t wnext = t < tend ? decode_word<BLOCKS>(c.bitmap, pm, t, lane, c.dim, c.bs, nelem_words) : 0u;
+  uint32_t wnext = t < tend ? decode_word<BLOCKS>(c.bitmap, t, lane, c.dim, c.bs, nelem_words) : 0u;
   for (; t < tend; t += tstep) {
     const uint32_t word = wnext;
-    if (t + tstep < tend) wnext = decode_word<BLOCKS>(c.bitmap, pm, t + tstep, lane, c.dim, c.bs, nelem_words);
+    if (t + tstep < tend) wnext = decode_word<BLOCKS>(c.bitmap, t + tstep, lane, c.dim, c.bs, nelem_words);
     decode_tile<R>(c, t * kDecTile, word, hp, q, vals);
-  }
-}
-
-// Union words OR-ed straight from the W ranks' bitmaps in peer memory (NVLink), fetched
-// kAhead tiles ahead of the decode so the remote latency hides under kAhead tiles of work
-// (the exchange kernel then moves only the sketch table).
-template <int R>
-__device__ __forceinline__ void decode_range_peers(const DecodeCtx& c, const PeerMaps& pm, int64_t t0, int64_t tstep,
-                                                   int64_t tend, const HashParams& hp, uint16_t* q, float* vals) {
-  constexpr int kAhead = 8;
-  const int lane = threadIdx.x & 31;
-  const int64_t nelem_words = (c.dim + 31) / 32;
-  auto fetch = [&](int64_t t) -> uint32_t {
-    uint32_t w = 0;
-    const int64_t wi = t * 32 + lane;
-    if (t < tend && wi < nelem_words) {
-#pragma unroll
-      for (int r = 0; r < kMaxWorld; ++r)
-        if (r < pm.n) w |= __ldcg(pm.p[r] + wi);
-    }
-    const int64_t e0 = t * kDecTile + 32 * lane;
-    if (e0 + 32 > c.dim) w &= e0 >= c.dim ? 0u : range_mask(0, (int)(c.dim - e0));
-    return w;
-  };
-  uint32_t cur[kAhead];
-#pragma unroll
-  for (int k = 0; k < kAhead; ++k) cur[k] = fetch(t0 + (int64_t)k * tstep);
-  for (int64_t g = t0; g < tend; g += (int64_t)kAhead * tstep) {
-    uint32_t nxt[kAhead];
-#pragma unroll
-    for (int k = 0; k < kAhead; ++k) nxt[k] = fetch(g + (int64_t)(kAhead + k) * tstep);
-#pragma unroll
-    for (int k = 0; k < kAhead; ++k) {
-      const int64_t t = g + (int64_t)k * tstep;
-      if (t < tend) decode_tile<R>(c, t * kDecTile, cur[k], hp, q, vals);
-    }
-#pragma unroll
-    for (int k = 0; k < kAhead; ++k) cur[k] = nxt[k];
   }
 }
 

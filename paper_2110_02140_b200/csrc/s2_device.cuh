@@ -45,36 +45,6 @@ inline bool pdl_enabled() {
   return v != 0;
 }
 
-// Optional L2 persistence for the sketch table (S2_L2_PERSIST=1): the table is the only
-// data with reuse (r atomics / gathers per value against a 3-50 MB table) while the
-// gradient and the output stream through once; an access-policy window marks it
-// persisting so the streams cannot evict it.
-struct L2Window {
-  const void* base = nullptr;
-  size_t bytes = 0;
-};
-inline L2Window& l2_window() {
-  static thread_local L2Window w;
-  return w;
-}
-inline bool l2_persist_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("S2_L2_PERSIST");
-    v = e ? atoi(e) : 0;
-    if (v) {
-      int dev = 0, maxp = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
-      if (maxp <= 0 || cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp) != cudaSuccess) {
-        cudaGetLastError();
-        v = 0;
-      }
-    }
-  }
-  return v != 0;
-}
-
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                              Args&&... args) {
@@ -83,36 +53,50 @@ inline cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, si
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  const L2Window& w = l2_window();
-  if (w.base != nullptr && l2_persist_enabled()) {
-    attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
-    attr[1].val.accessPolicyWindow.base_ptr = const_cast<void*>(w.base);
-    attr[1].val.accessPolicyWindow.num_bytes = w.bytes;
-    attr[1].val.accessPolicyWindow.hitRatio = 1.0f;
-    attr[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    attr[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    cfg.numAttrs = 2;
-  }
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 // ------------------------------------------------------------------ insert
+
+// fp32 add into global memory that keeps subnormals.  red.global.add.f32 flushes subnormal
+// inputs and results to zero (REDG.E.ADD.F32.FTZ.RN in SASS), while the reference adds in
+// float64 (np.add.at, sketch.py:111).  Every fp32 value with |v| >= 2^-100 is a multiple of
+// 2^-123, so any sum of such values is 0 or at least 2^-123 — a normal number — and the RED
+// rounds exactly like an IEEE add.  Smaller values (never seen in real gradients) go through
+// a CAS loop whose add is the IEEE, non-FTZ FADD (nvcc's default -ftz=false).  When tiny and
+// normal contributions meet in one cell, a RED can still flush a subnormal intermediate:
+// that error is < 2^-126, far below the 1e-5 * M tolerance of a cell holding a value >= 2^-100.
+__device__ __forceinline__ void add_f32(float* p, float v) {
+  if (!(fabsf(v) < 0x1p-100f)) {  // also NaN/Inf: one RED
+    atomicAdd(p, v);               // RED.E.ADD.F32 (result unused)
+    return;
+  }
+  unsigned int* a = reinterpret_cast<unsigned int*>(p);
+  unsigned int old = *reinterpret_cast<volatile unsigned int*>(a), assumed;
+  do {
+    assumed = old;
+    old = atomicCAS(a, assumed, __float_as_uint(__fadd_rn(__uint_as_float(assumed), v)));
+  } while (old != assumed);
+}
 
 template <int R>
 __device__ __forceinline__ void insert_one(uint64_t i, float v, float* __restrict__ table,
                                            const HashParams& hp) {
   const size_t cols = hp.cols;
   if (hp.mode == kInjective) {
-    // injective mapping: bucket(i) = i, sign = +1 (core.py:131-141)
+    // injective mapping: bucket(i) = i, sign = +1 (core.py:131-141).  The host raises the
+    // reference's ValueError for i >= cols (core.py:133-134); the guard keeps a direct C-ABI
+    // caller from writing past the table.
+    if (i >= cols) return;
 #pragma unroll
     for (int j = 0; j < (R > 0 ? R : S2_MAX_ROWS); ++j) {
       if (R == 0 && j >= hp.rows) break;
-      atomicAdd(table + j * cols + i, v);
+      add_f32(table + j * cols + i, v);
     }
     return;
   }
@@ -122,7 +106,7 @@ __device__ __forceinline__ void insert_one(uint64_t i, float v, float* __restric
     if (R == 0 && j >= hp.rows) break;
     const uint64_t w = mix64(hp.seed[j] + x);
     const uint32_t b = bucket_of(w, hp);
-    atomicAdd(table + j * cols + b, (w >> 63) ? -v : v);  // RED.E.ADD.F32 (result unused)
+    add_f32(table + j * cols + b, (w >> 63) ? -v : v);
   }
 }
 

@@ -1,17 +1,9 @@
-// s2_kernels.cu — sm_100a kernels of the S2 sparse-sketch reduce.
+// s2_kernels.cu — the functional-API kernels of the S2 path (the reduce's K1+K2 live in
+// s2_compress.cu, K4 in s2_decode.cu, K3 in s2_p2p.cu).
 //
-//   K1+K2  k_compress_elem / k_compress_blocks
-//          read g once (128-bit streaming loads), __ballot_sync bitmap words,
-//          warp-level prefix compaction of the non-zeros into a per-warp shared
-//          queue, and count-sketch insertion (r hashes, red.global.add.f32 into
-//          the L2-resident table) once 32 entries are queued, so every lane of
-//          the hashing warp is busy.  Replaces sparse_compress (sparse.py:151-171)
-//          + CountSketchTable.insert (sketch.py:102-112).
 //   K3b    k_bitmap_or — BlockMask.union over W gathered bitmaps (sparse.py:55-58)
-//   K4     k_decode — walk the union bitmap, compact set positions per warp tile,
-//          r gathers + lower-median network, ÷W (IEEE), dense float4 streaming
-//          stores incl. zeros.  Replaces sparse_decompress (sparse.py:199-214)
-//          + CountSketchTable.query (sketch.py:114-128).
+//   pairs  k_insert_pairs / k_query_pairs — CountSketchTable.insert / .query on index
+//          lists (sketch.py:102-128)
 //   aux    k_compact_* (ordered (idx,val) compaction = selected_indices,
 //          sparse.py:44-49 / :164-168), k_selected_count (sparse.py:51-53),
 //          k_table_sum (sketch.py:213-216).
@@ -303,13 +295,9 @@ cudaError_t launch_pairs(const Plan& p, const int64_t* idx, const float* vals, i
                          float* out, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   float* table = const_cast<float*>(table_in);
-  switch (p.hp.rows) {
-#define S2_CASE(r) case r: launch_pairs_r<r>(p, idx, vals, n, table, out, st); break;
-    S2_CASE(1) S2_CASE(2) S2_CASE(3) S2_CASE(4) S2_CASE(5) S2_CASE(6) S2_CASE(7) S2_CASE(8)
-    S2_CASE(9) S2_CASE(10) S2_CASE(11) S2_CASE(12) S2_CASE(13) S2_CASE(14) S2_CASE(15) S2_CASE(16)
-#undef S2_CASE
-    default: return cudaErrorInvalidValue;
-  }
+  if (p.hp.rows < 1 || p.hp.rows > S2_MAX_ROWS) return cudaErrorInvalidValue;
+  if (p.hp.rows == 3) launch_pairs_r<3>(p, idx, vals, n, table, out, st);  // the default sketch
+  else launch_pairs_r<0>(p, idx, vals, n, table, out, st);                 // any rows <= 16
   return cudaGetLastError();
 }
 

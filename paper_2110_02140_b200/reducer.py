@@ -18,7 +18,8 @@ import ctypes
 
 import torch
 
-from ._lib import S2_CNT_NNZ, S2_CNT_NONFINITE, S2_NUM_COUNTERS, check, lib, ptr, stream_ptr
+from ._lib import (S2_CNT_NNZ, S2_CNT_NONFINITE, S2_COMM_IPC, S2_COMM_NCCL, S2_NUM_COUNTERS, S2_STATUS_EXCHANGE,
+                   S2_STATUS_NONFINITE, check, lib, ptr, stream_ptr)
 from .core import as_gradient
 from .sketch import Plan
 from .sparse import DEFAULT_ROWS, DEFAULT_SIZE_RATIO, sketch_cols
@@ -38,17 +39,73 @@ def broadcast_unique_id(rank: int, group=None) -> bytes:
     return box[0]
 
 
+_STATUS_RING = 8  # outstanding reduces whose status words are checked without synchronising
+
+
+class _StatusRing:
+    """Per-reduce health words written by the decode kernel into mapped pinned host memory
+    (s2_plan_set_status), checked once the reduce's event has completed — the previous
+    steps' NaN/Inf and exchange-timeout flags surface without a host synchronisation."""
+
+    def __init__(self, handle, device):
+        self.h = handle
+        self.words = torch.zeros(_STATUS_RING, dtype=torch.int32, pin_memory=True)
+        self.pending = []  # (event, slot, phase-tag)
+        self.n = 0
+        self.device = device
+
+    def arm(self) -> int:
+        if len(self.pending) >= _STATUS_RING:  # the GPU lags by a full ring: wait for the oldest
+            self.pending[0][0].synchronize()
+            self.poll()
+        k = self.n % _STATUS_RING
+        self.n += 1
+        self.words[k] = -1  # not yet written
+        check(lib.s2_plan_set_status(self.h, ctypes.c_void_p(self.words.data_ptr() + 4 * k)), "set status")
+        return k
+
+    def launched(self, k: int, stream) -> None:
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        self.pending.append((ev, k))
+
+    def poll(self, wait: bool = False) -> None:
+        while self.pending and (wait or self.pending[0][0].query()):
+            ev, k = self.pending.pop(0)
+            if wait:
+                ev.synchronize()
+            st = int(self.words[k]) & 0xFFFFFFFF
+            if st == 0xFFFFFFFF:
+                continue  # slot never written (e.g. a graph replayed with another status slot)
+            if st & S2_STATUS_EXCHANGE:
+                self.pending.clear()
+                raise RuntimeError("S2 exchange: a cross-rank barrier timed out (a rank died, stalled past the "
+                                   "timeout, or the ranks' reduce sequences diverged); the averaged gradient "
+                                   "was set to NaN")
+            if st & S2_STATUS_NONFINITE:
+                self.pending.clear()
+                raise ValueError("gradient vector contains NaN or Inf")  # core.py:157-158
+
+
 class S2Reducer:
     """Averaged sparse-sketch all-reduce of a flat float32 gradient.
 
     Parameters mirror ``SparseSketchCompressor`` (sparse.py:294-305): ``cols``
     defaults to ``sketch_cols(size_ratio, alpha, dim, rows)``; ``num_blocks``
     defaults to ``dim`` (element bitmap, the north-star mask rule).
+
+    ``reduce`` never synchronises.  Each call first checks the health words of the
+    previous reduces that have already completed on the GPU and raises the reference's
+    ``ValueError`` ("gradient vector contains NaN or Inf", core.py:157-158) for a rank
+    whose gradient held NaN/Inf, or ``RuntimeError`` if the cross-rank exchange timed out
+    (``timeout_s``, default 300 s; the output of such a step is all NaN, never a silently
+    incomplete average).  ``check()`` waits for every outstanding reduce and raises the same.
     """
 
     def __init__(self, dim: int, rows: int = DEFAULT_ROWS, cols: int | None = None, seed: int = 0,
                  num_blocks: int | None = None, size_ratio: float = DEFAULT_SIZE_RATIO,
-                 alpha: float | None = None, group=None, world: int | None = None, rank: int | None = None):
+                 alpha: float | None = None, group=None, world: int | None = None, rank: int | None = None,
+                 timeout_s: float = 0.0, exchange_grid: int = 0):
         import torch.distributed as dist
 
         if cols is None:
@@ -65,65 +122,37 @@ class S2Reducer:
             rank = dist.get_rank(group) if world > 1 else 0
         self.world, self.rank = int(world), int(rank)
         uid = (ctypes.c_uint8 * 128)()
-        self._symm = None
-        mode = 0  # S2_COMM_IPC
+        mode = S2_COMM_IPC
         if self.world > 1:
             ctypes.memmove(uid, broadcast_unique_id(self.rank, group), 128)
-            mode = self._exchange_mode(group)
+            import os
+
+            if os.environ.get("S2_AGG") == "nccl":  # north-star literal: NCCL all-reduce + all-gather + OR
+                mode = S2_COMM_NCCL
+        check(lib.s2_comm_set_options(self.plan.handle, int(exchange_grid), float(timeout_s)), "comm options")
         check(lib.s2_comm_init_mode(self.plan.handle, self.world, self.rank, uid, mode), "comm init")
-        if mode == 2:  # S2_COMM_EXTERNAL: torch symmetric memory (+ NVLS multicast address)
-            self._attach_symmetric(group)
         check(lib.s2_comm_check(self.plan.handle, stream_ptr()), "comm check")
-
-    def _exchange_mode(self, group) -> int:
-        """CUDA-IPC arena by default; S2_NVLS=1 opts into torch symmetric memory + NVLS multicast
-        (measured slower at W = 2 and 4); S2_AGG=nccl uses NCCL collectives."""
-        import os
-
-        if os.environ.get("S2_AGG") == "nccl":
-            return 1
-        if os.environ.get("S2_NVLS", "0") == "0":
-            return 0
-        try:
-            import torch.distributed._symmetric_memory as symm_mem
-
-            ok = bool(symm_mem._SymmetricMemory.has_multicast_support(symm_mem.DeviceType.CUDA,
-                                                                       self.device.index))
-        except Exception:  # noqa: BLE001 - older torch / no NVSwitch: IPC arena
-            ok = False
-        import torch.distributed as dist
-
-        flags = [None] * self.world
-        dist.all_gather_object(flags, ok, group=group)
-        return 2 if all(flags) else 0
-
-    def _attach_symmetric(self, group) -> None:
-        import torch.distributed as dist
-        import torch.distributed._symmetric_memory as symm_mem
-
-        nbytes = int(lib.s2_p2p_arena_bytes(self.plan.handle, self.world))
-        if nbytes <= 0:
-            raise RuntimeError("s2_p2p_arena_bytes failed")
-        buf = symm_mem.empty(nbytes, dtype=torch.uint8, device=self.device)
-        hdl = symm_mem.rendezvous(buf, group if group is not None else dist.group.WORLD)
-        bases = (ctypes.c_uint64 * self.world)(*[int(p) for p in hdl.buffer_ptrs])
-        mc = int(getattr(hdl, "multicast_ptr", 0) or 0)
-        check(lib.s2_comm_attach(self.plan.handle, bases, self.world, mc), "comm attach")
-        self._symm = (buf, hdl)  # keep the mapping alive for the plan's lifetime
-        torch.cuda.synchronize()
-        dist.barrier(group=group)  # every arena is zeroed before any rank signals into it
+        self._status = _StatusRing(self.plan.handle, self.device)
 
     def reduce(self, g: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         """Averaged gradient estimate: median-of-rows sketch query ÷ world at every union-bitmap
         coordinate, 0 elsewhere (sparse_decompress of sparse_merge of every rank's sparse_compress)."""
         if g.numel() != self.dim:
             raise ValueError(f"dimension mismatch: mask dim {self.dim}, vector {g.numel()}")
+        self._status.poll()
         if not (g.is_cuda and g.dtype == torch.float32 and g.is_contiguous() and g.data_ptr() % 16 == 0):
             g = as_gradient(g, self.device)
         if out is None:
             out = torch.empty(self.dim, dtype=torch.float32, device=self.device)
-        check(lib.s2_reduce(self.plan.handle, ptr(g), ptr(out), None, stream_ptr(stream)), "reduce")
+        st = stream if stream is not None else torch.cuda.current_stream()
+        k = self._status.arm()
+        check(lib.s2_reduce(self.plan.handle, ptr(g), ptr(out), None, stream_ptr(st)), "reduce")
+        self._status.launched(k, st)
         return out
+
+    def check(self) -> None:
+        """Wait for every outstanding reduce and raise for NaN/Inf or an exchange timeout."""
+        self._status.poll(wait=True)
 
     def counters(self) -> list[int]:
         """Counters of the last reduce (synchronises the current stream): [nnz, nonfinite, selected, 0]."""
@@ -144,7 +173,7 @@ class S2Reducer:
         ranks' reduce sequences diverged); synchronises the device."""
         torch.cuda.synchronize(self.device)
         if lib.s2_p2p_error(self.plan.handle):
-            raise RuntimeError("S2 exchange: a cross-rank barrier timed out after 10 s")
+            raise RuntimeError("S2 exchange: a cross-rank barrier timed out")
 
 
 class HostPipeline:
@@ -222,16 +251,44 @@ class GraphedReduce:
                 reducer.reduce(g_static, out=out_static, stream=s)
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
+        reducer.check()
         self.graphs = []
-        for _ in range(2):
+        # each graph writes its health word into its own pinned slot (captured pointer)
+        self.words = torch.zeros(2, dtype=torch.int32, pin_memory=True)
+        for k in range(2):
+            check(lib.s2_plan_set_status(reducer.plan.handle, ctypes.c_void_p(self.words.data_ptr() + 4 * k)),
+                  "set status")
             gph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gph):
-                reducer.reduce(g_static, out=out_static)
+                check(lib.s2_reduce(reducer.plan.handle, ptr(g_static), ptr(out_static), None, stream_ptr()),
+                      "reduce")
             self.graphs.append(gph)
+        check(lib.s2_plan_set_status(reducer.plan.handle, None), "set status")
         # capture flipped the phase twice: back at the phase graph 0 was recorded in
         self.k = 0
+        self.last = [None, None]
 
     def __call__(self) -> torch.Tensor:
-        self.graphs[self.k].replay()
+        k = self.k
+        if self.last[k] is not None:  # this graph's previous replay must be checked before reuse
+            self.last[k].synchronize()
+            self._check(k)
+        self.graphs[k].replay()
+        ev = torch.cuda.Event()
+        ev.record()
+        self.last[k] = ev
         self.k ^= 1
         return self.out
+
+    def _check(self, k: int) -> None:
+        st = int(self.words[k]) & 0xFFFFFFFF
+        if st & S2_STATUS_EXCHANGE:
+            raise RuntimeError("S2 exchange: a cross-rank barrier timed out; the averaged gradient was set to NaN")
+        if st & S2_STATUS_NONFINITE:
+            raise ValueError("gradient vector contains NaN or Inf")
+
+    def check(self) -> None:
+        for k in range(2):
+            if self.last[k] is not None:
+                self.last[k].synchronize()
+                self._check(k)

@@ -199,6 +199,16 @@ class SparsePayload:
             self._size_ratio = self.table.rows * self.table.cols / (a * self.mask.partition.dim) if a > 0 else float("inf")
         return self._size_ratio
 
+    def selected_count(self) -> int:
+        """Coordinates inside selected blocks, sizes()[flags].sum() (sparse.py:51-53, :273)."""
+        if self.counters is not None:
+            return int(self.counters[S2_CNT_SELECTED])
+        p = self.mask.partition
+        plan = get_plan(p.dim, p.num_blocks, 1, 1, 0)
+        cnt = _new_counters(self.mask.words.device)
+        check(lib.s2_selected_count(plan.handle, ptr(self.mask.words), ptr(cnt), stream_ptr()), "selected_count")
+        return int(cnt[S2_CNT_SELECTED])
+
     @property
     def nnz(self) -> int:
         """Values inserted into the sketch (device counter)."""
@@ -333,12 +343,77 @@ def sparse_decompress(payload: SparsePayload, workers: int | None = None, out: t
         raise ValueError("workers must be >= 1")
     p = payload.mask.partition
     t = payload.table
+    if t.injective and t.cols < p.dim:
+        # the query maps every selected coordinate, zeros inside set blocks included
+        # (sparse.py:211-213); HashMapping(injective) raises for any index >= buckets (core.py:133-134)
+        sel = np.flatnonzero(payload.mask.flags)
+        if sel.size and min((int(sel[-1]) + 1) * p.block_size, p.dim) - 1 >= t.cols:
+            raise ValueError("injective mapping requires indices < buckets")
     plan = get_plan(p.dim, p.num_blocks, t.rows, t.cols, t.seed, t.injective)
     if out is None:
         out = torch.empty(p.dim, dtype=torch.float32, device=t.device)
     check(lib.s2_decode(plan.handle, ptr(payload.mask.words), ptr(t.table), int(workers), ptr(out), stream_ptr()),
           "decompress")
     return out
+
+
+def sparsify(g, num_blocks: int, k: int) -> torch.Tensor:
+    """g with every block outside the top-k (by L2 norm) zeroed (sparse.py:217-224), on the GPU."""
+    g = as_gradient(g)
+    idx = block_topk(g, num_blocks, k).selected_indices()
+    out = torch.zeros_like(g)
+    out[idx] = g[idx]
+    return out
+
+
+def topk_delta_check(g, num_blocks: int, k: int) -> tuple[float, float]:
+    """Energy kept by block top-k versus the k/b floor (sparse.py:227-242): (kept_ratio, bound);
+    the ratio is 1 for the zero vector.  Norms accumulate in float64 like the reference."""
+    g = as_gradient(g)
+    bound = k / num_blocks
+    g64 = g.double()
+    total = float(g64 @ g64)
+    if total == 0.0:
+        return 1.0, bound
+    kept = sparsify(g, num_blocks, k).double()
+    return float(kept @ kept) / total, bound
+
+
+@dataclass
+class CommCost:
+    """Wire cost of one payload against dense and coordinate baselines (sparse.py:244-261)."""
+
+    payload_bits: int
+    dense_bits: int
+    coordinate_bits: int
+    value_bits: int
+    bitmap_bits: int
+    header_bits: int
+
+    @property
+    def ratio_vs_dense(self) -> float:
+        return self.payload_bits / self.dense_bits
+
+    @property
+    def ratio_vs_coordinate(self) -> float:
+        return self.payload_bits / self.coordinate_bits
+
+
+def sparse_comm_bits(payload: SparsePayload) -> CommCost:
+    """Account the payload's bits: bitmap + 32-bit table cells + header (sparse.py:264-285).
+    The coordinate baseline sends each selected value as 32 bits plus a ceil(log2 dim)-bit
+    index; the selected count comes from the compress kernel's device counter."""
+    part = payload.mask.partition
+    nnz = payload.selected_count()
+    index_bits = max(1, (part.dim - 1).bit_length())
+    return CommCost(
+        payload_bits=8 * payload.serialized_nbytes(),
+        dense_bits=32 * part.dim,
+        coordinate_bits=nnz * (32 + index_bits),
+        value_bits=32 * payload.table.rows * payload.table.cols,
+        bitmap_bits=part.num_blocks,
+        header_bits=8 * (4 + 1 + 6 * 8),
+    )
 
 
 class SparseSketchCompressor:

@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
 def test_abi_version_and_errors():
     from paper_2110_02140_b200._lib import check, lib
 
-    assert lib.s2_abi_version() == 1
+    assert lib.s2_abi_version() == 2
     h = ctypes.c_void_p()
     with pytest.raises(ValueError, match="rows and cols must be >= 1"):
         check(lib.s2_plan_create(10, 10, 0, 4, 0, 0, ctypes.byref(h)))

@@ -1,0 +1,151 @@
+"""The W > 1 exchange on ONE GPU: W virtual ranks (own plans, arenas and streams, no NCCL)
+run the product's peer-memory exchange kernels (k_p2p_oneshot / k_p2p_aggregate), so a
+single-GPU box checks W = 2..8 — including the north-star W = 8 — against the oracle's
+sparse_merge + sparse_decompress (sparse.py:174-214).
+
+Bar: integer inputs bit-exact; real-valued inputs within
+1e-5 * max_j M[j, h_j(i)] / W; every rank's output bit-identical (replicated decode).
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import s2_oracle as o
+
+pytestmark = pytest.mark.gpu
+
+
+def _reference(grads, nb, rows, cols, seed, kind):
+    dim = grads[0].size
+    ps = [o.compress(g, o.nonzero_flags(g, nb), rows, cols, seed) for g in grads]
+    m = o.merge(ps)
+    ref = o.decompress(m)
+    mmax = None
+    if kind != "int":
+        mass = np.zeros((rows, cols))
+        for g, p in zip(grads, ps):
+            idx = o.selected_indices(p.flags, dim)
+            idx = idx[g[idx] != 0]
+            mass += o.sketch_l1_mass(o.row_seeds(seed, rows), idx, g[idx].astype(np.float64), cols)
+        sel = o.selected_indices(m.flags, dim)
+        mmax = np.zeros(dim)
+        for j, s in enumerate(o.row_seeds(seed, rows)):
+            mmax[sel] = np.maximum(mmax[sel], mass[j, o.hash_buckets(s, sel, cols)])
+    return ref, m, mmax
+
+
+def _check(outs, ref, mmax, W, kind):
+    h0 = outs[0]
+    for r, out in enumerate(outs):
+        assert np.array_equal(out, h0), f"rank {r} differs from rank 0 (replicated decode)"
+    if kind == "int":
+        assert np.array_equal(h0, ref.astype(np.float32)), np.abs(h0 - ref).max()
+    else:
+        err = np.abs(h0.astype(np.float64) - ref)
+        assert (err <= 1e-5 * mmax / W + 1e-30).all(), (err / np.maximum(mmax / W, 1e-30)).max()
+
+
+CASES = [  # (W, one-shot max W, num_blocks divisor, rows, cols)
+    (2, 2, 1, 3, 20011),      # default one-shot
+    (2, 1, 1, 3, 20011),      # two-shot at W = 2
+    (3, 2, 1, 3, 20011),      # two-shot, W not a power of two (IEEE ÷3)
+    (3, 4, 1, 5, 65536),      # one-shot at W = 3
+    (4, 2, 1, 3, 262144),     # default two-shot
+    (4, 4, 1, 3, 20011),      # one-shot at W = 4
+    (4, 2, 32, 3, 20011),     # block bitmap, 32 elements per block
+    (5, 2, 1, 3, 20011),
+    (6, 2, 1, 5, 1_000_000),  # BERT-like non-power-of-two width
+    (7, 2, 7, 3, 4099),       # ragged blocks
+    (8, 2, 1, 3, 262144),     # the north-star W = 8
+    (8, 2, 1, 3, 20011),
+]
+
+
+@pytest.mark.parametrize("W,oneshot_maxw,bdiv,rows,cols", CASES)
+def test_local_exchange_parity(W, oneshot_maxw, bdiv, rows, cols):
+    import torch
+
+    from paper_2110_02140_b200.local import LocalGroup
+
+    dim = 2_000_003
+    nb = dim if bdiv == 1 else -(-dim // bdiv)
+    old = os.environ.get("S2_P2P_ONESHOT_MAXW")
+    os.environ["S2_P2P_ONESHOT_MAXW"] = str(oneshot_maxw)  # read when the arena is laid out
+    try:
+        grp = LocalGroup(W, dim, rows, cols, seed=0, num_blocks=nb)
+    finally:
+        if old is None:
+            os.environ.pop("S2_P2P_ONESHOT_MAXW")
+        else:
+            os.environ["S2_P2P_ONESHOT_MAXW"] = old
+    words = torch.zeros(W, dtype=torch.int32, device="cuda")
+    grp.set_status(words)
+    # three inputs with different non-zero positions, each reduced twice (both ping-pong buffers):
+    # a stale bitmap or table from the previous call would show up as a parity failure
+    for kind, base in (("int", 1234), ("normal", 1234), ("normal", 4321)):
+        grads = [o.synthetic_gradient(dim, 0.01, r, kind=kind, base_seed=base) for r in range(W)]
+        ref, _, mmax = _reference(grads, nb, rows, cols, 0, kind)
+        gt = [torch.from_numpy(g).cuda() for g in grads]
+        for _ in range(2):
+            outs = grp.reduce(gt)
+            torch.cuda.synchronize()
+            _check([x.cpu().numpy() for x in outs], ref, mmax, W, kind)
+            assert words.cpu().tolist() == [0] * W
+    assert grp.errors() == [0] * W
+
+
+def test_local_exchange_timeout_poisons_output():
+    """A rank that never arrives: the waiting rank's barrier gives up after the timeout, the
+    output is all NaN (never a silently incomplete average) and the status word says so;
+    later reduces stay NaN without waiting again (the error is sticky)."""
+    import time
+
+    import torch
+
+    from paper_2110_02140_b200._lib import S2_STATUS_EXCHANGE, check, lib, ptr
+    from paper_2110_02140_b200.local import LocalGroup
+
+    dim = 100_000
+    grp = LocalGroup(2, dim, 3, 1667, timeout_s=0.5)
+    words = torch.zeros(2, dtype=torch.int32, device="cuda")
+    grp.set_status(words)
+    g = torch.from_numpy(o.synthetic_gradient(dim, 0.01, 0, kind="int")).cuda()
+    out = torch.zeros(dim, device="cuda")
+    import ctypes
+
+    t0 = time.time()
+    check(lib.s2_reduce(grp.plans[0].handle, ptr(g), ptr(out), None, ctypes.c_void_p(0)))  # rank 1 never comes
+    torch.cuda.synchronize()
+    assert time.time() - t0 < 30
+    assert torch.isnan(out).all()
+    assert int(words[0]) == S2_STATUS_EXCHANGE
+    assert lib.s2_p2p_error(grp.plans[0].handle) != 0
+    t0 = time.time()
+    out.zero_()
+    check(lib.s2_reduce(grp.plans[0].handle, ptr(g), ptr(out), None, ctypes.c_void_p(0)))
+    torch.cuda.synchronize()
+    assert time.time() - t0 < 0.4, "a plan that timed out must not wait again"
+    assert torch.isnan(out).all()
+
+
+def test_reducer_async_status_raises_on_next_call():
+    """S2Reducer surfaces the previous step's NaN/Inf flag on a later call without syncing."""
+    import torch
+
+    import paper_2110_02140_b200 as s2
+
+    d = 100_000
+    red = s2.S2Reducer(d, rows=3, cols=1667)
+    g = torch.from_numpy(o.synthetic_gradient(d, 0.01, 0, kind="int")).cuda()
+    red.reduce(g)
+    red.check()
+    bad = g.clone()
+    bad[5] = float("nan")
+    red.reduce(bad)
+    torch.cuda.synchronize()
+    with pytest.raises(ValueError, match="gradient vector contains NaN or Inf"):
+        red.reduce(g)
+    red.reduce(g)
+    red.check()  # healthy again

@@ -20,18 +20,10 @@ def ngpus():
 VARIANTS = {
     "ipc": {},                                 # default: CUDA-IPC arena, one-shot (W=2) / two-shot (W>2)
     "ipc_twoshot": {"S2_P2P_ONESHOT_MAXW": "1"},
-    "nvls": {"S2_NVLS": "1"},                  # torch symmetric memory + multimem in-switch reduce
-    "nccl": {"S2_AGG": "nccl"},                # NCCL all-reduce + all-gather + OR kernel
-    "fused": {"S2_FUSED": "1"},                # exchange + decode in one kernel
-    "bitmap_in_decode": {"S2_P2P_BITMAP_IN_DECODE_MAXW": "8"},  # decode ORs peer bitmaps over NVLink
+    "ipc_oneshot": {"S2_P2P_ONESHOT_MAXW": "4"},
+    "nccl": {"S2_AGG": "nccl"},                # NCCL all-reduce + all-gather + OR kernel (north-star literal)
     "graph": {"S2_CHECK_GRAPH": "1"},          # CUDA-graph replay of the whole reduce
-    "hier": {"S2_P2P_HIER": "1"},              # hierarchical cross-rank barriers
-    "csig": {"S2_P2P_COMPRESS_SIGNAL": "1"},   # compress kernels signal completion to the peers
-    "pipe": {"S2_P2P_PIPE": "1", "S2_P2P_ONESHOT_MAXW": "1"},  # pipelined two-shot, per-peer waits
     "blocks": {"S2_CHECK_NUM_BLOCKS": "62500"},  # block bitmap (b < d, 32 elements per block)
-    "push": {"S2_P2P_BITMAP_PUSH_MAXW": "8"},  # compress stores its bitmap into the peers' inboxes
-    "push_graph": {"S2_P2P_BITMAP_PUSH_MAXW": "8", "S2_CHECK_GRAPH": "1"},
-    "coop": {"S2_P2P_COOP": "1", "S2_P2P_GRID": "148"},  # cooperative launch, one CTA per SM
 }
 
 
@@ -52,7 +44,8 @@ def test_dist_reduce_parity(world, variant):
 
 
 def test_ddp_comm_hook_trains():
-    """S2 as a DDP comm hook with error feedback (casq.ef_step semantics) on an embedding model."""
+    """S2 as a DDP comm hook on an embedding model: one bucket without error feedback, and several
+    rebuilt buckets with error feedback (casq.ef_step semantics against the merged estimate)."""
     if ngpus() < 2:
         pytest.skip("needs 2 GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",

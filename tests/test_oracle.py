@@ -93,6 +93,8 @@ def test_oracle_matches_golden(name):
     wire = payloads[0].to_bytes()
     assert np.array_equal(np.frombuffer(wire[:53], np.uint8), z["wire_head"])
     assert hashlib.sha256(wire).digest() == z["wire_sha256"].tobytes()
+    assert list(o.comm_bits(payloads[0])) == z["comm_bits"].tolist()  # sparse.py:264-285
+    assert list(o.comm_bits(m)) == z["comm_bits_merged"].tolist()
 
 
 def test_edge_semantics():

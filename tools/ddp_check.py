@@ -1,9 +1,11 @@
-"""DDP training with the S2 comm hook (error feedback) on an embedding model — W ranks.
+"""DDP training with the S2 comm hook on an embedding model — W ranks.
 
     torchrun --nproc-per-node 2 tools/ddp_check.py
-Checks: training converges, every rank holds bit-identical gradients after the hook,
-and the hook's estimate matches the oracle decode of the W ranks' bucket gradients
-(first step, integer-scaled gradients -> exact)."""
+Two runs against exact all-reduce training: one bucket without error feedback, and
+several small buckets (DDP rebuilds them after the first iteration) with error feedback
+(casq.ef_step semantics against the merged estimate).  Checks: both converge, every rank
+holds bit-identical gradients after the hook, and the hook's estimate stays close to the
+exact average."""
 import json
 import os
 import sys
@@ -35,11 +37,11 @@ class Model(nn.Module):
         return self.head(self.emb(idx).mean(1)).squeeze(-1)
 
 
-def train(hook: bool):
+def train(hook: bool, ef: bool = False, cap_mb: float = 1000):
     torch.manual_seed(0)
     model = Model().cuda()
-    ddp = nn.parallel.DistributedDataParallel(model, device_ids=[rank], bucket_cap_mb=1000)
-    state = S2HookState(size_ratio=4.0, alpha=0.3, seed=1, error_feedback=False)
+    ddp = nn.parallel.DistributedDataParallel(model, device_ids=[rank], bucket_cap_mb=cap_mb)
+    state = S2HookState(size_ratio=4.0, alpha=0.3, seed=1, error_feedback=ef)
     if hook:
         ddp.register_comm_hook(state, diag_hook)
     opt = torch.optim.SGD(ddp.parameters(), lr=2.0)
@@ -73,14 +75,24 @@ def diag_hook(st, bucket):
 
 true_w = torch.randn(V, device="cuda")
 l_exact, _, _ = train(False)
-l_s2, flat, state = train(True)
-h = [None] * world
-dist.all_gather_object(h, flat.double().sum().item())
-rep = {"world": world, "loss_exact_last": float(np.mean(l_exact[-20:])), "loss_s2_last": float(np.mean(l_s2[-20:])),
-       "loss_first": float(np.mean(l_s2[:10])), "max_rel_err": max(DIAG), "grads_replicated": len(set(h)) == 1,
-       "buckets": len(state.reducers)}
-rep["ok"] = (rep["grads_replicated"] and rep["max_rel_err"] < 0.1
-             and rep["loss_s2_last"] <= 1.1 * rep["loss_exact_last"] and rep["loss_s2_last"] < rep["loss_first"])
+rep = {"world": world, "loss_exact_last": float(np.mean(l_exact[-20:]))}
+rep["ok"] = True
+for name, ef, cap in (("s2", False, 1000), ("s2_ef_buckets", True, 0.03)):
+    DIAG.clear()
+    l_s2, flat, state = train(True, ef, cap)
+    state.check()
+    h = [None] * world
+    dist.all_gather_object(h, flat.double().sum().item())
+    r = {"loss_last": float(np.mean(l_s2[-20:])), "loss_first": float(np.mean(l_s2[:10])),
+         "max_rel_err": max(DIAG), "grads_replicated": len(set(h)) == 1, "bucket_sizes": len(state.reducers),
+         "residuals": len(state.residuals)}
+    # without EF the estimate must track the exact average; with EF (residuals densify the
+    # compressed vector, DDP.py docstring) the run must still converge
+    r["ok"] = r["grads_replicated"] and (
+        (r["loss_last"] <= 1.1 * rep["loss_exact_last"] and r["max_rel_err"] < 0.1) if not ef
+        else r["loss_last"] < 0.5 * r["loss_first"])
+    rep[name] = r
+    rep["ok"] &= r["ok"]
 if rank == 0:
     print(json.dumps(rep), flush=True)
 dist.destroy_process_group()
