@@ -7,9 +7,9 @@ One step = one full reduce of one synthetic gradient per rank: compress (bitmap 
 compaction + count-sketch insert) -> sketch all-reduce + bitmap all-gather/OR
 (N > 1, NCCL over NVLink) -> median decode (÷N) into a dense fp32 gradient.
 
-Prints ONE JSON line (rank 0).  ``value`` = whole-job dense-equivalent GB/s =
-N * 4*d / t_reduce (t = max over ranks, CUDA events, K steps); ``ms_per_step``
-= t_reduce.  ``e2e`` repeats the measurement through the same C-ABI call with
+Prints ONE JSON line (rank 0).  ``value`` = dense-equivalent GB/s reduced per GPU
+= 4*d / t_reduce (BASELINE.json's metric; t = max over ranks, CUDA events, K steps);
+``job_GBps`` = N * 4*d / t_reduce, the whole job; ``ms_per_step`` = t_reduce.  ``e2e`` repeats the measurement through the same C-ABI call with
 pinned HOST buffers, H2D of the gradient and D2H of the result inside the timed
 region.  ``--impl reference`` times the CPU reference path (the NumPy oracle
 port of sketchgrad.sparse, bit-identical to the as-shipped reference) on all the
@@ -50,6 +50,8 @@ CONFIGS = {
     # union densities a W=2 / W=4 reduce decodes (dev configs for single-GPU decode tuning)
     "resnet50_d2": dict(dim=25_600_000, alpha=0.02, rows=3, cols=262_144, label="ResNet-50-sized, 98% sparse"),
     "resnet50_d4": dict(dim=25_600_000, alpha=0.04, rows=3, cols=262_144, label="ResNet-50-sized, 96% sparse"),
+    # 1 - 0.99^8: the union a W = 8 reduce decodes (single-GPU proxy for the north-star W = 8 decode)
+    "resnet50_d8": dict(dim=25_600_000, alpha=0.0773, rows=3, cols=262_144, label="ResNet-50-sized, 92.3% sparse"),
     "oracle1m": dict(dim=1_000_000, alpha=0.01, rows=3, cols=16_384, label="1M fp32, 99% sparse (configs[0])"),
 }
 N_ROTATE = 4  # distinct gradient buffers cycled through: N_ROTATE * 4d bytes > 126 MB L2
@@ -175,9 +177,10 @@ def reference_arm(args, cfg):
     W = args.gpus
     d = cfg["dim"]
     dt, done, cores = _time_reference(cfg, W, args.warmup, args.steps, args.ref_budget)
-    value = W * 4 * d / dt / 1e9
+    value = 4 * d / dt / 1e9  # per GPU: each step reduces W ranks' d-element gradients
     line = {
-        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": W,
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "job_GBps": round(W * value, 4),
+        "unit": "GB/s", "n_gpus": W,
         "steps": done, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": _config_json(args, cfg),
@@ -191,11 +194,29 @@ def reference_arm(args, cfg):
 
 
 def cpu_baseline(cfg, budget_s=10.0):
-    """Oracle port timed on this host's cores (rank 0, N=1): compress + merge + decompress of one gradient."""
+    """Oracle port timed on this host's cores (rank 0, N=1): compress + merge + decompress of one
+    gradient; plus the reference's call structure as shipped (single-threaded NumPy, Python slice
+    loops for index extraction) at configs[0] = 1M / 99 % / 3 x 16384."""
     dt, n, cores = _time_reference(cfg, 1, 1, 50, budget_s)
-    return {"value": round(4 * cfg["dim"] / dt / 1e9, 4), "unit": "GB/s", "cores": cores, "kind": "port",
-            "sample": f"{n} full reduces (W=1) of the {cfg['dim']}-element workload, chunked over {cores} "
-                      f"worker processes (oracle/parallel.py); numpy {np.__version__}"}
+    out = {"value": round(4 * cfg["dim"] / dt / 1e9, 4), "unit": "GB/s", "cores": cores, "kind": "port",
+           "sample": f"{n} full reduces (W=1) of the {cfg['dim']}-element workload, chunked over {cores} "
+                     f"worker processes (oracle/parallel.py); numpy {np.__version__}"}
+    from oracle import s2_oracle as o
+
+    c0 = CONFIGS["oracle1m"]
+    g = o.synthetic_gradient(c0["dim"], c0["alpha"], 0)
+    o.reduce_as_shipped([g], c0["rows"], c0["cols"], 0)  # warm-up
+    t0, k = time.perf_counter(), 0
+    while k < 3 or (time.perf_counter() - t0 < 5.0 and k < 20):
+        o.reduce_as_shipped([g], c0["rows"], c0["cols"], 0)
+        k += 1
+    dts = (time.perf_counter() - t0) / k
+    out["as_shipped"] = {"value": round(4 * c0["dim"] / dts / 1e9, 5), "unit": "GB/s", "ms_per_step": round(dts * 1e3, 1),
+                         "cores": 1, "kind": "port-as-shipped",
+                         "sample": f"{k} reduces (W=1) of configs[0] (1M fp32, 99 % sparse, 3x16384) through "
+                                   "oracle.reduce_as_shipped: the reference's call structure incl. its Python "
+                                   "slice loops (core.py:195-200, sparse.py:44-49), one process, one core"}
+    return out
 
 
 def _rows_gradient_np(cfg, rank=0):
@@ -355,7 +376,7 @@ def ours(args, cfg):
         e1.record(stream)
         barrier()
         ms_dense = max_over_ranks(e0.elapsed_time(e1) / kd)
-        dense = {"ms_per_step": round(ms_dense, 5), "value": round(world * 4 * d / (ms_dense * 1e-3) / 1e9, 2),
+        dense = {"ms_per_step": round(ms_dense, 5), "value": round(4 * d / (ms_dense * 1e-3) / 1e9, 2),
                  "unit": "GB/s", "op": f"torch.distributed.all_reduce (NCCL, SUM) of {d} fp32, device-resident"}
         del buf
     barrier()
@@ -375,10 +396,17 @@ def ours(args, cfg):
     alg = {"compress": B + words_bytes + table_bytes, "decode": words_bytes + table_bytes + B}
     dom = max(("compress", "decode"), key=lambda k: phases[k])
     ach = alg[dom] / (phases[dom] * 1e-3) / 1e9
-    traffic = None
+    traffic, ncu = None, None
     tfile = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tfile):
-        traffic = json.load(open(tfile)).get(f"{args.config}:{dom}")
+        tj = json.load(open(tfile))
+        traffic = tj.get(f"{args.config}:{dom}")
+        # the same kernel's duration from the committed ncu launch list (cold L2, serialised)
+        nd = tj.get(f"{args.config}:{dom}:ncu_us")
+        if nd:
+            na = alg[dom] / (nd * 1e-6) / 1e9
+            ncu = {"us": nd, "achieved": round(na, 1), "frac": round(na / hbm_peak, 4),
+                   "source": tj.get("_source", "profiles/traffic.json")}
     phase_out = {}
     for k in ("compress", "decode"):
         a = alg[k] / (phases[k] * 1e-3) / 1e9
@@ -389,17 +417,18 @@ def ours(args, cfg):
         phase_out["aggregate"] = {"ms": round(phases["aggregate"], 5),
                                   "bus_GB/s": round(bus / (phases["aggregate"] * 1e-3) / 1e9, 1),
                                   "bus_bytes": bus}
-    value = world * B / (ms * 1e-3) / 1e9
+    value = B / (ms * 1e-3) / 1e9  # per GPU (BASELINE.json metric); job_GBps = world * value
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms, 5), "per_gpu_GBps": round(B / (ms * 1e-3) / 1e9, 2),
+        "warmup": args.warmup, "ms_per_step": round(ms, 5), "job_GBps": round(world * value, 2),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": _config_json(args, cfg),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(ach / hbm_peak, 4), "traffic": traffic, "peak_kind": peak_kind,
-                     "bytes_per_launch": alg[dom]},
+                     "bytes_per_launch": alg[dom], "timing": "CUDA events around the kernel inside the step",
+                     "ncu": ncu},
         "phases": phase_out,
-        "e2e": {"value": round(world * B / (ms_e2e * 1e-3) / 1e9, 3), "unit": "GB/s", "ms_per_step": round(ms_e2e, 4),
+        "e2e": {"value": round(B / (ms_e2e * 1e-3) / 1e9, 3), "unit": "GB/s", "ms_per_step": round(ms_e2e, 4),
                 "h2d_bytes_per_step": B, "d2h_bytes_per_step": B,
                 "path": "HostPipeline.submit -> S2Reducer.reduce (C-ABI s2_reduce); pinned host buffers; "
                         "H2D/D2H of every step inside the timed region (CUDA events: first H2D start to "

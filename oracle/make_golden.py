@@ -155,6 +155,20 @@ def case(core, sparse, name, dim, alpha, rows, cols, W, kind, num_blocks=None, s
     np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **d)
 
 
+def topk_delta(sparse):
+    """sparsify / topk_delta_check (sparse.py:217-242) on a few block layouts."""
+    rng = np.random.default_rng(5)
+    gs, outs, checks, params = [], [], [], []
+    for d, nb, k in ((10_007, 100, 7), (4096, 4096, 300), (1000, 7, 3)):
+        g = (rng.standard_normal(d) * (rng.random(d) < 0.3)).astype(np.float32)
+        gs.append(np.pad(g, (0, 10_007 - d)))
+        outs.append(np.pad(sparse.sparsify(g.astype(np.float64), nb, k), (0, 10_007 - d)))
+        checks.append(sparse.topk_delta_check(g.astype(np.float64), nb, k))
+        params.append((d, nb, k))
+    np.savez_compressed(os.path.join(OUT, "topk_delta.npz"), grads=np.stack(gs), sparsified=np.stack(outs),
+                        checks=np.array(checks), params=np.array(params))
+
+
 def _comm(c):
     return np.array([c.payload_bits, c.dense_bits, c.coordinate_bits, c.value_bits, c.bitmap_bits, c.header_bits],
                     dtype=np.int64)
@@ -165,6 +179,7 @@ def main():
     os.makedirs(OUT, exist_ok=True)
     hash_kat(core)
     tiny(sketch)
+    topk_delta(sparse)
     # configs[0]: the oracle case, 1M / 99% / 3x16384 / W=1
     case(core, sparse, "s2_1m_w1", 1_000_000, 0.01, 3, 16384, 1, "normal")
     # mergeability (acceptance #7) at W=2,4,8; non-pow2 cols

@@ -144,6 +144,47 @@ def selected_indices(flags, dim: int) -> np.ndarray:
     return idx[idx < dim].astype(np.int64)
 
 
+def selected_indices_as_shipped(flags, dim: int) -> np.ndarray:
+    """The reference's own index extraction, restated loop for loop for timing the CPU path as
+    shipped: BlockPartition.slices() builds one slice object per block
+    (core.py:195-200) and selected_indices concatenates an arange per selected block
+    (sparse.py:44-49).  Same result as ``selected_indices``; ~100x slower at b = d."""
+    flags = np.asarray(flags, dtype=bool)
+    nb = flags.size
+    size = block_size(dim, nb)
+    slices = [slice(min(b * size, dim), min((b + 1) * size, dim)) for b in range(nb)]
+    picked = [np.arange(s.start, s.stop) for b, s in enumerate(slices) if flags[b]]
+    if not picked:
+        return np.zeros(0, dtype=np.int64)
+    return np.concatenate(picked).astype(np.int64)
+
+
+def reduce_as_shipped(grads, rows: int, cols: int, seed: int) -> np.ndarray:
+    """One W-rank reduce with the reference's call structure and element bitmap (b = d):
+    per rank BlockMask(part, g != 0) + sparse_compress (sparse.py:151-171), sparse_merge as a
+    left fold (:174-196), sparse_decompress (:199-214) — every index extraction through the
+    as-shipped slice loop.  Timing only; results equal decompress(merge(compress(...)))."""
+    seeds = row_seeds(seed, rows)
+    dim = grads[0].size
+    merged, flags_u, W = None, None, len(grads)
+    for g in grads:
+        g = as_gradient(g)
+        flags = g != 0
+        table = np.zeros((rows, cols), dtype=np.float64)
+        idx = selected_indices_as_shipped(flags, dim)
+        if idx.size:
+            vals = g[idx]
+            nz = vals != 0.0
+            sketch_insert(table, seeds, idx[nz], vals[nz], cols)
+        merged = table if merged is None else merged + table
+        flags_u = flags if flags_u is None else flags_u | flags
+    out = np.zeros(dim, dtype=np.float64)
+    idx = selected_indices_as_shipped(flags_u, dim)
+    if idx.size:
+        out[idx] = sketch_query(merged, seeds, idx, cols) / W
+    return out
+
+
 def selected_fraction(flags, dim: int) -> float:
     """alpha = selected coordinates / dim (sparse.py:51-53)."""
     flags = np.asarray(flags, dtype=bool)
@@ -188,6 +229,27 @@ def block_topk(g, num_blocks: int, k: int) -> np.ndarray:
     flags = np.zeros(num_blocks, dtype=bool)
     flags[order[:k]] = True
     return flags
+
+
+def sparsify(g, num_blocks: int, k: int) -> np.ndarray:
+    """Zero everything outside the top-k blocks (sparse.py:217-224)."""
+    g = as_gradient(g)
+    flags = block_topk(g, num_blocks, k)
+    out = np.zeros_like(g)
+    idx = selected_indices(flags, g.size)
+    out[idx] = g[idx]
+    return out
+
+
+def topk_delta_check(g, num_blocks: int, k: int) -> tuple:
+    """(|sparsify(g)|^2 / |g|^2, k/b), 1 for the zero vector (sparse.py:227-242)."""
+    g = as_gradient(g)
+    bound = k / num_blocks
+    total = float(g @ g)
+    if total == 0.0:
+        return 1.0, bound
+    kept = sparsify(g, num_blocks, k)
+    return float(kept @ kept) / total, bound
 
 
 # ---------------------------------------------------------------- sketch

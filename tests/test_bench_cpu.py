@@ -38,3 +38,15 @@ def test_reference_arm_torchrun_n2():
                        env=dict(os.environ, OMP_NUM_THREADS="1"))
     assert r.returncode == 0, r.stderr[-2000:]
     _check(r.stdout, 2)
+
+
+def test_cpu_baseline_reports_as_shipped():
+    """The ours-arm cpu_baseline carries the oracle port on all cores and the as-shipped call
+    structure (single core, Python slice loops) at configs[0]."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    cb = bench.cpu_baseline(bench.CONFIGS["oracle1m"], budget_s=1.0)
+    assert cb["kind"] == "port" and cb["value"] > 0 and cb["cores"] >= 1
+    a = cb["as_shipped"]
+    assert a["kind"] == "port-as-shipped" and a["cores"] == 1 and 0 < a["value"] < cb["value"]

@@ -444,3 +444,49 @@ def test_random_shapes_bit_exact(s2):
         assert np.array_equal(host(m.table.table), om.table.astype(np.float32)), trial
         out = host(s2.sparse_decompress(m))
         assert np.array_equal(out, o.decompress(om).astype(np.float32)), (trial, dim, nb, rows, cols, W)
+
+
+def test_injective_decompress_rejects_out_of_range(s2):
+    """Injective mapping with cols < dim (core.py:131-135): a block mask whose selected coordinates
+    reach past cols raises the reference's ValueError at decompress (the query maps every selected
+    coordinate, zeros included, sparse.py:211-213) instead of reading past the table."""
+    d = 1000
+    g = np.zeros(d, np.float32)
+    g[[3, 7]] = [1.0, 2.0]
+    part = s2.BlockPartition(d, 10)  # 100-element blocks
+    ok = s2.sparse_compress(cuda(g), s2.BlockMask(part, [True] + [False] * 9), 1, 100, 0, injective=True)
+    assert np.array_equal(host(s2.sparse_decompress(ok))[:100], g[:100])
+    bad = s2.sparse_compress(cuda(g), s2.BlockMask(part, [True, True] + [False] * 8), 1, 150, 0, injective=True)
+    with pytest.raises(ValueError, match="injective mapping requires indices < buckets"):
+        s2.sparse_decompress(bad)
+
+
+def test_sparsify_topk_delta_golden(s2):
+    """sparsify / topk_delta_check (sparse.py:217-242) against the live-reference fixture."""
+    z = load("topk_delta")
+    for (d, nb, k), g, sp, chk in zip(z["params"], z["grads"], z["sparsified"], z["checks"]):
+        out = host(s2.sparsify(cuda(g[:d]), int(nb), int(k)))
+        assert np.array_equal(out, sp[:d].astype(np.float32))
+        kept, bound = s2.topk_delta_check(cuda(g[:d]), int(nb), int(k))
+        assert bound == chk[1] and abs(kept - chk[0]) <= 1e-12 and kept >= bound
+
+
+def test_block_topk_near_ties(s2):
+    """Blocks holding permutations of the same values have equal norms in exact arithmetic; the
+    GPU's float64 norm (warp-shuffle order) and np.linalg.norm (BLAS order) may round such near-
+    ties differently.  Every block whose reference norm is separated from the k-th norm by more
+    than 8 ulp must agree; only blocks inside that band may swap (documented in DESIGN.md §5)."""
+    rng = np.random.default_rng(31)
+    for trial in range(20):
+        nb, bs = int(rng.integers(50, 400)), int(rng.integers(3, 200))
+        base = rng.standard_normal(bs).astype(np.float32)
+        g = np.concatenate([rng.permutation(base) * (1.0 if rng.random() < 0.7 else rng.random() * 2)
+                            for _ in range(nb)]).astype(np.float32)
+        k = int(rng.integers(1, nb))
+        got = s2.block_topk(cuda(g), nb, k).flags
+        ref = o.block_topk(g, nb, k)
+        norms = np.array([np.linalg.norm(g[b * bs:(b + 1) * bs].astype(np.float64)) for b in range(nb)])
+        kth = np.sort(norms)[::-1][k - 1]
+        band = np.abs(norms - kth) <= 8 * np.spacing(kth)
+        assert int(got.sum()) == k
+        assert np.array_equal(got[~band], ref[~band]), trial

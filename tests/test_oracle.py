@@ -97,6 +97,23 @@ def test_oracle_matches_golden(name):
     assert list(o.comm_bits(m)) == z["comm_bits_merged"].tolist()
 
 
+def test_sparsify_topk_delta_golden():
+    z = load("topk_delta")
+    for (d, nb, k), g, sp, chk in zip(z["params"], z["grads"], z["sparsified"], z["checks"]):
+        assert np.array_equal(o.sparsify(g[:d], int(nb), int(k)), sp[:d])
+        assert o.topk_delta_check(g[:d], int(nb), int(k)) == tuple(chk)
+
+
+def test_as_shipped_restatement():
+    """The loop-for-loop restatement bench.py times as the as-shipped reference equals the oracle."""
+    for W, d, nb in ((1, 20_000, 20_000), (3, 30_011, 30_011)):
+        grads = [o.synthetic_gradient(d, 0.02, r) for r in range(W)]
+        ref = o.decompress(o.merge([o.compress(g, g != 0, 3, 97, 5) for g in grads]))
+        assert np.array_equal(o.reduce_as_shipped(grads, 3, 97, 5), ref)
+    f = np.random.default_rng(0).random(1000) < 0.3
+    assert np.array_equal(o.selected_indices_as_shipped(f, 9_999), o.selected_indices(f, 9_999))
+
+
 def test_edge_semantics():
     z = load("s2_edge37")
     # -0.0 at index 32 is not a non-zero (sparse.py:167); all-zero worker has an empty mask
