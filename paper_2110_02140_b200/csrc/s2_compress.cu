@@ -39,16 +39,18 @@ __device__ __forceinline__ void flush_full(uint32_t* qi, float* qv, int& qn, int
   __syncwarp();
 }
 
-__device__ __forceinline__ void load_tile(float4 (&v)[8], const float* __restrict__ g, int64_t t, int64_t dim,
+template <int KF>
+__device__ __forceinline__ void load_tile(float4 (&v)[KF], const float* __restrict__ g, int64_t t, int64_t dim,
                                           int lane) {
-  const int64_t base = t * kTile;
-  if (base + kTile <= dim) {
+  constexpr int kT = 128 * KF;
+  const int64_t base = t * kT;
+  if (base + kT <= dim) {
     const float4* g4 = reinterpret_cast<const float4*>(g) + (base >> 2) + lane;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = __ldcs(g4 + k * 32);
+    for (int k = 0; k < KF; ++k) v[k] = __ldcs(g4 + k * 32);
   } else {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < KF; ++k) {
       const int64_t e = base + k * 128 + lane * 4;
       v[k].x = e + 0 < dim ? g[e + 0] : 0.f;
       v[k].y = e + 1 < dim ? g[e + 1] : 0.f;
@@ -58,20 +60,24 @@ __device__ __forceinline__ void load_tile(float4 (&v)[8], const float* __restric
   }
 }
 
-template <int R, int MODE>
-__global__ void __launch_bounds__(kThreads, 2)
+// KF = float4 chunks per lane per warp tile (kCompressKF = 8: 1024 elements, 127 registers,
+// 2 CTAs per SM).
+template <int R, int MODE, int KF>
+__global__ void __launch_bounds__(kThreads, KF == 8 ? 2 : 4)
 k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __restrict__ bitmap,
            float* __restrict__ table, unsigned long long* __restrict__ counters,
            const __grid_constant__ HashParams hp) {
+  constexpr int kT = 128 * KF;  // elements per warp tile
+  constexpr int kW = 4 * KF;    // bitmap words per warp tile
   constexpr int kCap = 32 + kQFast;
   __shared__ uint32_t s_qi[kWarps][kCap];
   __shared__ float s_qv[kWarps][kCap];
-  __shared__ __align__(16) float4 s_tile[kWarps][kTile / 4];  // value stage of the current tile
+  __shared__ __align__(16) float4 s_tile[kWarps][kT / 4];  // value stage of the current tile
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   uint32_t* qi = s_qi[wib];
   float* qv = s_qv[wib];
-  const int64_t ntiles = (dim + kTile - 1) / kTile;
+  const int64_t ntiles = (dim + kT - 1) / kT;
   const int64_t nelem_words = (dim + 31) / 32;
   const int64_t nw = (int64_t)gridDim.x * kWarps;
   const int src_grp = 8 * (lane & 3);  // transpose: word L gathers lanes 8(L&3)..+7
@@ -86,34 +92,37 @@ k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __res
   griddep_wait();  // g may be written by the caller's previous kernel
   griddep_launch_dependents();
   int64_t t = (int64_t)blockIdx.x * kWarps + wib;
-  float4 vn[8];
-  if (t < ntiles) load_tile(vn, g, t, dim, lane);
+  float4 vn[KF];
+  if (t < ntiles) load_tile<KF>(vn, g, t, dim, lane);
 #pragma unroll 1
   for (; t < ntiles; t += nw) {
-    const int64_t base = t * kTile;
-    float4 v[8];
+    const int64_t base = t * kT;
+    float4 v[KF];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = vn[k];
-    if (t + nw < ntiles) load_tile(vn, g, t + nw, dim, lane);  // prefetch the next tile
+    for (int k = 0; k < KF; ++k) v[k] = vn[k];
+    if (t + nw < ntiles) load_tile<KF>(vn, g, t + nw, dim, lane);  // prefetch the next tile
     // non-zero flags (-0.0 == 0 is not a non-zero, sparse.py:167)
     uint32_t m = 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < KF; ++k) {
       m |= ((uint32_t)(v[k].x != 0.f) << (4 * k)) | ((uint32_t)(v[k].y != 0.f) << (4 * k + 1)) |
            ((uint32_t)(v[k].z != 0.f) << (4 * k + 2)) | ((uint32_t)(v[k].w != 0.f) << (4 * k + 3));
     }
     if (MODE == 2) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) fin += 0.f * v[k].x + 0.f * v[k].y + 0.f * v[k].z + 0.f * v[k].w;
-      // selection word of elements base+32L..+31, then the inverse transpose into m's layout
-      uint32_t mword = bs == 1 ? ((t * 32 + lane) < nelem_words ? __ldg(bitmap + t * 32 + lane) : 0u)
-                               : expand_blocks(bitmap, base + 32 * lane, dim, bs);
-      const int64_t e0 = base + 32 * lane;
-      if (e0 + 32 > dim) mword &= e0 >= dim ? 0u : range_mask(0, (int)(dim - e0));
+      for (int k = 0; k < KF; ++k) fin += 0.f * v[k].x + 0.f * v[k].y + 0.f * v[k].z + 0.f * v[k].w;
+      // selection word of elements base+32L..+31 (lanes L < kW), then the inverse transpose into m's layout
+      uint32_t mword = 0;
+      if (lane < kW) {
+        mword = bs == 1 ? ((t * kW + lane) < nelem_words ? __ldg(bitmap + t * kW + lane) : 0u)
+                        : expand_blocks(bitmap, base + 32 * lane, dim, bs);
+        const int64_t e0 = base + 32 * lane;
+        if (e0 + 32 > dim) mword &= e0 >= dim ? 0u : range_mask(0, (int)(dim - e0));
+      }
       sel += __popc(mword);
       uint32_t msel = 0;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
+      for (int k = 0; k < KF; ++k) {
         const uint32_t mk = __shfl_sync(kFull, mword, 4 * k + (lane >> 3));
         msel |= ((mk >> ((lane & 7) * 4)) & 0xFu) << (4 * k);
       }
@@ -143,7 +152,7 @@ k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __res
         int pos = qn + incl - cnt;
         float4* st = s_tile[wib];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) st[k * 32 + lane] = v[k];
+        for (int k = 0; k < KF; ++k) st[k * 32 + lane] = v[k];
         __syncwarp();
         const float* sf = reinterpret_cast<const float*>(st);
         for (uint32_t mm = m; mm; mm &= mm - 1u) {
@@ -160,7 +169,7 @@ k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __res
         // dense tile: append chunk by chunk (<= 128 per chunk), flushing in between
         const uint32_t lt = lanemask_lt();
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < KF; ++k) {
           const uint32_t nib = (m >> (4 * k)) & 0xFu;
           const uint32_t b0 = __ballot_sync(kFull, nib & 1u);
           const uint32_t b1 = __ballot_sync(kFull, nib & 2u);
@@ -179,10 +188,10 @@ k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __res
       }
     }
     if (MODE == 0) {
-      const int64_t wi = t * 32 + lane;
-      if (wi < nelem_words) bitmap[wi] = word;
+      const int64_t wi = t * kW + lane;
+      if (lane < kW && wi < nelem_words) bitmap[wi] = word;
     } else if (MODE == 1) {
-      if (word) {  // OR the flags of every block this 32-element span touches
+      if (lane < kW && word) {  // OR the flags of every block this 32-element span touches
         const int64_t e0 = base + 32 * lane;
         const int64_t e_end = e0 + 32 < dim ? e0 + 32 : dim;
         int64_t b = e0 / bs, s = e0;
@@ -218,21 +227,36 @@ k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __res
 
 // =================================================================== launchers
 
+// float4 per lane per warp tile.  KF = 4 (512-element tiles, 64 registers, 32 warps per SM)
+// measured slower than KF = 8: compress alone 30.8 vs 24.8 µs at the ResNet-50 config, the
+// ResNet step 46.9 vs 42.0 µs (profiles/r02_ab_kf.txt): the per-tile fixed work (scan,
+// transpose, queue bookkeeping) doubles per byte while the bytes in flight stay the same.
+constexpr int kCompressKF = 8;
+
+template <int R, int KF>
+static cudaError_t launch_compress_rk(const Plan& p, const float* g, uint32_t* bitmap, float* table,
+                                      unsigned long long* counters, int mode, cudaStream_t st) {
+  const int64_t ntiles = (p.dim + 128 * KF - 1) / (128 * KF);
+  static int per_sm = -1;  // S2_COMPRESS_CTAS_PER_SM: grid = SMs x this (> resident -> extra waves)
+  if (per_sm < 0) {
+    const char* e = getenv("S2_COMPRESS_CTAS_PER_SM");
+    per_sm = e && atoi(e) > 0 ? atoi(e) : 0;
+  }
+  const int grid = grid_for(ntiles, per_sm > 0 ? per_sm : (KF == 8 ? 2 : 4));
+  if (mode == S2_MASK_GIVEN)
+    return launch_ex(k_compress<R, 2, KF>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table, counters,
+                     p.hp);
+  if (p.block_size == 1)
+    return launch_ex(k_compress<R, 0, KF>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table, counters,
+                     p.hp);
+  return launch_ex(k_compress<R, 1, KF>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table, counters,
+                   p.hp);
+}
+
 template <int R>
 static cudaError_t launch_compress_r(const Plan& p, const float* g, uint32_t* bitmap, float* table,
                                      unsigned long long* counters, int mode, cudaStream_t st) {
-  const int64_t ntiles = (p.dim + kTile - 1) / kTile;
-  static int per_sm = -1;  // S2_COMPRESS_CTAS_PER_SM: grid = SMs x this (> 2 -> extra waves)
-  if (per_sm < 0) {
-    const char* e = getenv("S2_COMPRESS_CTAS_PER_SM");
-    per_sm = e && atoi(e) > 0 ? atoi(e) : 2;
-  }
-  const int grid = grid_for(ntiles, per_sm);
-  if (mode == S2_MASK_GIVEN)
-    return launch_ex(k_compress<R, 2>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table, counters, p.hp);
-  if (p.block_size == 1)
-    return launch_ex(k_compress<R, 0>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table, counters, p.hp);
-  return launch_ex(k_compress<R, 1>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table, counters, p.hp);
+  return launch_compress_rk<R, kCompressKF>(p, g, bitmap, table, counters, mode, st);
 }
 
 cudaError_t launch_compress(const Plan& p, const float* g, uint32_t* bitmap, float* table,

@@ -37,11 +37,14 @@ __device__ __forceinline__ float lower_median(float (&e)[R]) {
 // R > 0: compile-time row count.  R == 0: any hp.rows <= S2_MAX_ROWS — the missing rows are
 // +inf, which sort last, so element (rows-1)/2 of the sorted 16 is the lower median.
 template <int R>
-__device__ __forceinline__ float query_one(uint64_t i, const float* __restrict__ table,
-                                           const HashParams& hp) {
-  constexpr int N = R > 0 ? R : S2_MAX_ROWS;
+__host__ __device__ constexpr int est_rows() { return R > 0 ? R : S2_MAX_ROWS; }
+
+// the r signed bucket values s_j(i) T[j, h_j(i)] of index i
+template <int R>
+__device__ __forceinline__ void query_estimates(uint64_t i, const float* __restrict__ table, const HashParams& hp,
+                                                float (&e)[est_rows<R>()]) {
+  constexpr int N = est_rows<R>();
   const size_t cols = hp.cols;
-  float e[N];
   if (hp.mode == kInjective) {
     // i >= cols is rejected on the host (core.py:133-134); the guard keeps reads in bounds
 #pragma unroll
@@ -60,9 +63,15 @@ __device__ __forceinline__ float query_one(uint64_t i, const float* __restrict__
       e[j] = (w >> 63) ? -t : t;
     }
   }
+}
+
+// lower median (element (r-1)/2 of the sorted estimates, sketch.py:127-128)
+template <int R>
+__device__ __forceinline__ float median_of(float (&e)[est_rows<R>()], const HashParams& hp) {
   if constexpr (R > 0) {
     return lower_median<R>(e);
   } else {
+    constexpr int N = S2_MAX_ROWS;
 #pragma unroll
     for (int p = 0; p < N; ++p) {
 #pragma unroll
@@ -79,6 +88,13 @@ __device__ __forceinline__ float query_one(uint64_t i, const float* __restrict__
       if (j == (hp.rows - 1) / 2) m = e[j];
     return m;
   }
+}
+
+template <int R>
+__device__ __forceinline__ float query_one(uint64_t i, const float* __restrict__ table, const HashParams& hp) {
+  float e[est_rows<R>()];
+  query_estimates<R>(i, table, hp, e);
+  return median_of<R>(e, hp);
 }
 
 template <bool BLOCKS>
@@ -133,6 +149,9 @@ __device__ __forceinline__ void decode_tile(const DecodeCtx& c, int64_t base, ui
   pre -= cnt;
   for (uint32_t w = word; w; w &= w - 1u) q[pre++] = (uint16_t)(lane * 32 + (__ffs(w) - 1));
   __syncwarp();
+  // Queries one per lane per round.  Two queries per lane with all 2r gathers in flight before
+  // either median was measured slower at every union density (decode 24.3 -> 25.0 µs at 1 %,
+  // 33.6 -> 35.2 at 4 %, 45.8 -> 47.4 at 7.7 %, profiles/r02_ab_decode_pairs.txt).
   for (int s = lane; s < total; s += 32) {
     const int pos = q[s];
     // IEEE division: sparse.py:213 divides the float64 query by workers; x*2^-k is exact
