@@ -324,6 +324,7 @@ static int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 // Arena layout (identical on every rank):
 //   tables[2] | bitmaps[2] | unions[2] | flags_a[W*8G] | flags_b[W*8G] | epochs[8G] | error | tsum[2]?
+//   | inbox[2]? (push exchange)
 // (flag and epoch slots for exchange grids of up to 8 CTAs per SM)
 static int64_t layout_p2p(s2_plan* plan, int W, int G) {
   const int64_t cells = round_up((int64_t)plan->p.hp.rows * plan->p.hp.cols, 4 * W);
@@ -346,6 +347,10 @@ static int64_t layout_p2p(s2_plan* plan, int W, int G) {
   const int oneshot_maxw = os_env ? atoi(os_env) : 2;
   a.oneshot = (W <= oneshot_maxw && W <= 4) ? 1 : 0;
   for (int k = 0; k < 2; ++k) a.off_tsum[k] = a.oneshot ? take(cells * 4) : a.off_table[k];
+  const char* pe = getenv("S2_P2P_PUSH");
+  a.push = pe ? atoi(pe) : 0;
+  // inbox: one-shot W slots of the whole table + bitmap, two-shot W slots of one slice each
+  for (int k = 0; k < 2; ++k) a.off_inbox[k] = a.push ? take((a.oneshot ? W : 1) * (cells + words) * 4) : -1;
   a.cells = cells;
   a.words = words;
   a.world = W;

@@ -63,7 +63,7 @@ __device__ __forceinline__ void load_tile(float4 (&v)[KF], const float* __restri
 // KF = float4 chunks per lane per warp tile (kCompressKF = 8: 1024 elements, 127 registers,
 // 2 CTAs per SM).
 template <int R, int MODE, int KF>
-__global__ void __launch_bounds__(kThreads, KF == 8 ? 2 : 4)
+__global__ void __launch_bounds__(kThreads, 2)
 k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __restrict__ bitmap,
            float* __restrict__ table, unsigned long long* __restrict__ counters,
            const __grid_constant__ HashParams hp) {
@@ -231,6 +231,8 @@ k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __res
 // measured slower than KF = 8: compress alone 30.8 vs 24.8 µs at the ResNet-50 config, the
 // ResNet step 46.9 vs 42.0 µs (profiles/r02_ab_kf.txt): the per-tile fixed work (scan,
 // transpose, queue bookkeeping) doubles per byte while the bytes in flight stay the same.
+// KF = 8 squeezed to 80 registers for 3 CTAs (24 warps) per SM spills and is slower still:
+// compress 26.2 -> 37.0 µs at ResNet-50, 237 -> 370 µs at GPT-2-M 99 % (profiles/r02_ab_occ.txt).
 constexpr int kCompressKF = 8;
 
 template <int R, int KF>
@@ -242,7 +244,7 @@ static cudaError_t launch_compress_rk(const Plan& p, const float* g, uint32_t* b
     const char* e = getenv("S2_COMPRESS_CTAS_PER_SM");
     per_sm = e && atoi(e) > 0 ? atoi(e) : 0;
   }
-  const int grid = grid_for(ntiles, per_sm > 0 ? per_sm : (KF == 8 ? 2 : 4));
+  const int grid = grid_for(ntiles, per_sm > 0 ? per_sm : 2);
   if (mode == S2_MASK_GIVEN)
     return launch_ex(k_compress<R, 2, KF>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table, counters,
                      p.hp);

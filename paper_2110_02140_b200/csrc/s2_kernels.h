@@ -64,6 +64,8 @@ struct P2PArgs {
   int64_t words;  // bitmap words, padded to a multiple of 4 * world
   int world, rank, cur;
   int oneshot;                    // 1: one-shot exchange (single barrier), 0: two-shot
+  int push;                       // 1: data pushed into the peers' inboxes before each flag (else pulled after)
+  int64_t off_inbox[2];           // push: W slots (one-shot: whole table+bitmap; two-shot: one slice)
   unsigned long long timeout_ns;  // cross-rank barrier spin limit (then: sticky error, NaN output)
   unsigned long long* trace;      // optional: per-CTA globaltimer stamps [G][8] (S2_P2P_TRACE=1)
 };

@@ -58,15 +58,22 @@ __device__ __forceinline__ uint64_t globaltimer() {
       a.trace[(int64_t)blockIdx.x * 8 + (slot)] = globaltimer();                \
   } while (0)
 
-// CTA b of this rank <-> CTA b of every rank (flag slot [rank * G + b] of each rank's array).
+// CTA b announces epoch `ep` to CTA b of every rank (flag slot [rank * G + b] of each rank's
+// array): every write of this CTA — local, or remote stores into a peer's inbox — happens-
+// before the release (bar.sync is cumulative), so a peer that acquires the flag sees them.
 template <int W>
-__device__ __forceinline__ void cross_rank_barrier(const P2PArgs& a, int64_t off_flags, uint32_t ep) {
-  __syncthreads();  // the CTA's writes happen-before thread q's release (bar.sync is cumulative)
+__device__ __forceinline__ void signal_ranks(const P2PArgs& a, int64_t off_flags, uint32_t ep) {
+  __syncthreads();
+  if (threadIdx.x < W)
+    st_release_sys(reinterpret_cast<uint32_t*>(a.base[threadIdx.x] + off_flags) + a.rank * gridDim.x + blockIdx.x, ep);
+}
+
+// CTA b waits until CTA b of every rank has announced `ep` in this rank's flag array.
+template <int W>
+__device__ __forceinline__ void wait_ranks(const P2PArgs& a, int64_t off_flags, uint32_t ep) {
   if (threadIdx.x < W) {
     const int q = threadIdx.x;
     uint32_t* err = reinterpret_cast<uint32_t*>(a.base[a.rank] + a.off_error);
-    uint32_t* remote = reinterpret_cast<uint32_t*>(a.base[q] + off_flags) + a.rank * gridDim.x + blockIdx.x;
-    st_release_sys(remote, ep);
     const uint32_t* mine = reinterpret_cast<const uint32_t*>(a.base[a.rank] + off_flags) + q * gridDim.x + blockIdx.x;
     if (*reinterpret_cast<volatile uint32_t*>(err) == 0u) {  // after a timeout the epochs no longer pair up
       uint64_t t0 = 0;
@@ -84,6 +91,13 @@ __device__ __forceinline__ void cross_rank_barrier(const P2PArgs& a, int64_t off
     }
   }
   __syncthreads();
+}
+
+// CTA b of this rank <-> CTA b of every rank
+template <int W>
+__device__ __forceinline__ void cross_rank_barrier(const P2PArgs& a, int64_t off_flags, uint32_t ep) {
+  signal_ranks<W>(a, off_flags, ep);
+  wait_ranks<W>(a, off_flags, ep);
 }
 
 // chunk [lo, hi) of n vectors for CTA b of G
@@ -251,9 +265,149 @@ __global__ void __launch_bounds__(kP2PThreads) k_p2p_oneshot(const __grid_consta
   S2_TRACE(4);
 }
 
+// ============================================================ push exchange (S2_P2P_PUSH=1)
+//
+// The same sums and ORs, but every rank STORES its data into the peers' inboxes (remote NVLink
+// writes) before announcing it, instead of announcing first and letting the peers pull: a rank
+// that finishes its compress early moves its data while the late ranks are still compressing,
+// and each flag wait is followed by local reads only.
+//   one-shot: push my whole table+bitmap chunk into inbox slot [me] of every peer, signal, wait,
+//             then sum / OR the W copies (own buffers + W-1 inbox slots, all local) in rank order.
+//   two-shot: push slice q of my chunk into inbox slot [me] of rank q, signal, wait; reduce my
+//             slice from the W copies in rank order (in place); push the reduced slice into every
+//             peer's table / union, signal, wait.
+template <int W>
+__global__ void __launch_bounds__(kP2PThreads) k_p2p_push_oneshot(const __grid_constant__ P2PArgs a) {
+  __shared__ uint32_t s_ep;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic launch: compress must be complete
+  S2_TRACE(0);
+  const uint32_t ep = next_epoch(a, &s_ep);
+  const int me = a.rank, cur = a.cur;
+  const int64_t t4 = a.cells / 4, w4 = a.words / 4, slot = (t4 + w4) * 16;
+  int64_t lo, hi;
+  chunk_of(t4 + w4, lo, hi);
+  const int64_t in_me = a.off_inbox[cur] + me * slot;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += kP2PThreads) {
+    const int64_t off = i < t4 ? a.off_table[cur] + i * 16 : a.off_bitmap[cur] + (i - t4) * 16;
+    const uint4 v = __ldcg(reinterpret_cast<const uint4*>(a.base[me] + off));
+#pragma unroll
+    for (int q = 0; q < W; ++q)
+      if (q != me) __stcg(reinterpret_cast<uint4*>(a.base[q] + in_me + i * 16), v);
+  }
+  S2_TRACE(1);
+  signal_ranks<W>(a, a.off_flags_a, ep);
+  wait_ranks<W>(a, a.off_flags_a, ep);
+  S2_TRACE(2);
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  constexpr int B = p2p_batch<W>();
+  for (int64_t i0 = lo + threadIdx.x; i0 < hi; i0 += (int64_t)B * kP2PThreads) {
+    uint4 v[B][W];
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      const int64_t i = i0 + (int64_t)k * kP2PThreads;
+      if (i < hi) {
+        const int64_t own = i < t4 ? a.off_table[cur] + i * 16 : a.off_bitmap[cur] + (i - t4) * 16;
+#pragma unroll
+        for (int q = 0; q < W; ++q)
+          v[k][q] = __ldcg(reinterpret_cast<const uint4*>(
+              a.base[me] + (q == me ? own : a.off_inbox[cur] + q * slot + i * 16)));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      const int64_t i = i0 + (int64_t)k * kP2PThreads;
+      if (i >= hi) continue;
+      uint4 s = v[k][0];
+      if (i < t4) {
+#pragma unroll
+        for (int q = 1; q < W; ++q) s = add4(s, v[k][q]);
+        *reinterpret_cast<uint4*>(a.base[me] + a.off_tsum[cur] + i * 16) = s;
+      } else {
+#pragma unroll
+        for (int q = 1; q < W; ++q) s = or4(s, v[k][q]);
+        *reinterpret_cast<uint4*>(a.base[me] + a.off_union[cur] + (i - t4) * 16) = s;
+      }
+    }
+  }
+  __syncthreads();
+  S2_TRACE(4);
+}
+
+template <int W>
+__global__ void __launch_bounds__(kP2PThreads) k_p2p_push_twoshot(const __grid_constant__ P2PArgs a) {
+  __shared__ uint32_t s_ep;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic launch: compress must be complete
+  S2_TRACE(0);
+  const uint32_t ep = next_epoch(a, &s_ep);
+  const int me = a.rank, cur = a.cur;
+  const int64_t t4 = a.cells / 4 / W, w4 = a.words / 4 / W, slot = (t4 + w4) * 16;  // per slice
+  int64_t lo, hi;
+  chunk_of(t4 + w4, lo, hi);
+  // vector i of slice s in this rank's table / bitmap (local) and union
+  auto src = [&](int sl, int64_t i) { return i < t4 ? a.off_table[cur] + (sl * t4 + i) * 16
+                                                    : a.off_bitmap[cur] + (sl * w4 + i - t4) * 16; };
+  auto dst = [&](int sl, int64_t i) { return i < t4 ? a.off_table[cur] + (sl * t4 + i) * 16
+                                                    : a.off_union[cur] + (sl * w4 + i - t4) * 16; };
+  // reduce-scatter, push: slice q of my chunk -> inbox slot [me] of rank q
+  for (int64_t i = lo + threadIdx.x; i < hi; i += kP2PThreads) {
+    uint4 v[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q)
+      if (q != me) v[q] = __ldcg(reinterpret_cast<const uint4*>(a.base[me] + src(q, i)));
+#pragma unroll
+    for (int q = 0; q < W; ++q)
+      if (q != me) __stcg(reinterpret_cast<uint4*>(a.base[q] + a.off_inbox[cur] + me * slot + i * 16), v[q]);
+  }
+  S2_TRACE(1);
+  signal_ranks<W>(a, a.off_flags_a, ep);
+  wait_ranks<W>(a, a.off_flags_a, ep);
+  S2_TRACE(2);
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // reduce my slice in rank order (own copy + W-1 inbox slots, all local), then all-gather, push
+  for (int64_t i = lo + threadIdx.x; i < hi; i += kP2PThreads) {
+    uint4 v[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q)
+      v[q] = __ldcg(reinterpret_cast<const uint4*>(
+          a.base[me] + (q == me ? src(me, i) : a.off_inbox[cur] + q * slot + i * 16)));
+    uint4 s = v[0];
+    if (i < t4) {
+#pragma unroll
+      for (int q = 1; q < W; ++q) s = add4(s, v[q]);
+    } else {
+#pragma unroll
+      for (int q = 1; q < W; ++q) s = or4(s, v[q]);
+    }
+    const int64_t o = dst(me, i);
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+      if (q == me) *reinterpret_cast<uint4*>(a.base[me] + o) = s;
+      else __stcg(reinterpret_cast<uint4*>(a.base[q] + o), s);
+    }
+  }
+  S2_TRACE(3);
+  signal_ranks<W>(a, a.off_flags_b, ep);
+  wait_ranks<W>(a, a.off_flags_b, ep);
+  S2_TRACE(4);
+}
+
 cudaError_t launch_p2p_aggregate(const P2PArgs& a, int grid, cudaStream_t st) {
   const void* fn = nullptr;
-  if (a.oneshot) {
+  if (a.push) {
+    switch (a.world * 2 + a.oneshot) {
+      case 5: fn = (const void*)k_p2p_push_oneshot<2>; break;
+      case 7: fn = (const void*)k_p2p_push_oneshot<3>; break;
+      case 9: fn = (const void*)k_p2p_push_oneshot<4>; break;
+      case 4: fn = (const void*)k_p2p_push_twoshot<2>; break;
+      case 6: fn = (const void*)k_p2p_push_twoshot<3>; break;
+      case 8: fn = (const void*)k_p2p_push_twoshot<4>; break;
+      case 10: fn = (const void*)k_p2p_push_twoshot<5>; break;
+      case 12: fn = (const void*)k_p2p_push_twoshot<6>; break;
+      case 14: fn = (const void*)k_p2p_push_twoshot<7>; break;
+      case 16: fn = (const void*)k_p2p_push_twoshot<8>; break;
+      default: return cudaErrorInvalidValue;
+    }
+  } else if (a.oneshot) {
     switch (a.world) {
       case 2: fn = (const void*)k_p2p_oneshot<2>; break;
       case 3: fn = (const void*)k_p2p_oneshot<3>; break;

@@ -47,39 +47,49 @@ def _check(outs, ref, mmax, W, kind):
         assert (err <= 1e-5 * mmax / W + 1e-30).all(), (err / np.maximum(mmax / W, 1e-30)).max()
 
 
-CASES = [  # (W, one-shot max W, num_blocks divisor, rows, cols)
-    (2, 2, 1, 3, 20011),      # default one-shot
-    (2, 1, 1, 3, 20011),      # two-shot at W = 2
-    (3, 2, 1, 3, 20011),      # two-shot, W not a power of two (IEEE ÷3)
-    (3, 4, 1, 5, 65536),      # one-shot at W = 3
-    (4, 2, 1, 3, 262144),     # default two-shot
-    (4, 4, 1, 3, 20011),      # one-shot at W = 4
-    (4, 2, 32, 3, 20011),     # block bitmap, 32 elements per block
-    (5, 2, 1, 3, 20011),
-    (6, 2, 1, 5, 1_000_000),  # BERT-like non-power-of-two width
-    (7, 2, 7, 3, 4099),       # ragged blocks
-    (8, 2, 1, 3, 262144),     # the north-star W = 8
-    (8, 2, 1, 3, 20011),
+CASES = [  # (W, one-shot max W, num_blocks divisor, rows, cols, push)
+    (2, 2, 1, 3, 20011, 0),      # default one-shot
+    (2, 1, 1, 3, 20011, 0),      # two-shot at W = 2
+    (3, 2, 1, 3, 20011, 0),      # two-shot, W not a power of two (IEEE ÷3)
+    (3, 4, 1, 5, 65536, 0),      # one-shot at W = 3
+    (4, 2, 1, 3, 262144, 0),     # default two-shot
+    (4, 4, 1, 3, 20011, 0),      # one-shot at W = 4
+    (4, 2, 32, 3, 20011, 0),     # block bitmap, 32 elements per block
+    (5, 2, 1, 3, 20011, 0),
+    (6, 2, 1, 5, 1_000_000, 0),  # BERT-like non-power-of-two width
+    (7, 2, 7, 3, 4099, 0),       # ragged blocks
+    (8, 2, 1, 3, 262144, 0),     # the north-star W = 8
+    (8, 2, 1, 3, 20011, 0),
+    # push exchange (S2_P2P_PUSH=1): data stored into the peers' inboxes before each flag
+    (2, 2, 1, 3, 20011, 1),
+    (3, 4, 1, 5, 65536, 1),
+    (4, 4, 32, 3, 20011, 1),
+    (2, 1, 1, 3, 20011, 1),
+    (4, 2, 1, 3, 262144, 1),
+    (7, 2, 7, 3, 4099, 1),
+    (8, 2, 1, 3, 262144, 1),
 ]
 
 
-@pytest.mark.parametrize("W,oneshot_maxw,bdiv,rows,cols", CASES)
-def test_local_exchange_parity(W, oneshot_maxw, bdiv, rows, cols):
+@pytest.mark.parametrize("W,oneshot_maxw,bdiv,rows,cols,push", CASES)
+def test_local_exchange_parity(W, oneshot_maxw, bdiv, rows, cols, push):
     import torch
 
     from paper_2110_02140_b200.local import LocalGroup
 
     dim = 2_000_003
     nb = dim if bdiv == 1 else -(-dim // bdiv)
-    old = os.environ.get("S2_P2P_ONESHOT_MAXW")
-    os.environ["S2_P2P_ONESHOT_MAXW"] = str(oneshot_maxw)  # read when the arena is laid out
+    env = {"S2_P2P_ONESHOT_MAXW": str(oneshot_maxw), "S2_P2P_PUSH": str(push)}  # read at arena layout
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
     try:
         grp = LocalGroup(W, dim, rows, cols, seed=0, num_blocks=nb)
     finally:
-        if old is None:
-            os.environ.pop("S2_P2P_ONESHOT_MAXW")
-        else:
-            os.environ["S2_P2P_ONESHOT_MAXW"] = old
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k)
+            else:
+                os.environ[k] = v
     words = torch.zeros(W, dtype=torch.int32, device="cuda")
     grp.set_status(words)
     # three inputs with different non-zero positions, each reduced twice (both ping-pong buffers):

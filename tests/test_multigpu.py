@@ -21,6 +21,8 @@ VARIANTS = {
     "ipc": {},                                 # default: CUDA-IPC arena, one-shot (W=2) / two-shot (W>2)
     "ipc_twoshot": {"S2_P2P_ONESHOT_MAXW": "1"},
     "ipc_oneshot": {"S2_P2P_ONESHOT_MAXW": "4"},
+    "push": {"S2_P2P_PUSH": "1"},              # data pushed into the peers' inboxes before each flag
+    "push_twoshot": {"S2_P2P_PUSH": "1", "S2_P2P_ONESHOT_MAXW": "1"},
     "nccl": {"S2_AGG": "nccl"},                # NCCL all-reduce + all-gather + OR kernel (north-star literal)
     "graph": {"S2_CHECK_GRAPH": "1"},          # CUDA-graph replay of the whole reduce
     "blocks": {"S2_CHECK_NUM_BLOCKS": "62500"},  # block bitmap (b < d, 32 elements per block)

@@ -7,8 +7,8 @@
 //   dsmem   atom.shared::cluster.add.f32 into a table distributed over the shared memory of
 //           a thread-block cluster (16 CTAs x 192 KB = 3 MB: the ResNet-50 sketch fits one
 //           cluster) — the only privatisation that holds a 3 MB table on chip
-// Every thread draws `per_thread` pseudo-random (cell, value) pairs with the same mix64 hash
-// as the sketch.  Build + run on a B200:
+// Every thread draws `per_thread` pseudo-random (cell, +-1) pairs (xorshift32, multiply-high
+// range reduction — cheap, so the rates reflect the memory system, not the index math).  Build + run on a B200:
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 tools/atomics_bench.cu -o /tmp/atomics_bench
 //   /tmp/atomics_bench
 #include <cooperative_groups.h>
@@ -18,17 +18,24 @@
 
 namespace cg = cooperative_groups;
 
-__device__ __forceinline__ uint64_t mix64(uint64_t z) {
-  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-  return z ^ (z >> 31);
+// cheap per-thread random stream (xorshift32) and multiply-high range reduction: a few integer
+// ops per draw, so the rates below measure the memory system, not the index arithmetic
+__device__ __forceinline__ uint32_t xs32(uint32_t& s) {
+  s ^= s << 13;
+  s ^= s >> 17;
+  s ^= s << 5;
+  return s;
+}
+__device__ __forceinline__ uint32_t cell_of(uint32_t r, uint32_t cells) { return __umulhi(r, cells); }
+__device__ __forceinline__ uint32_t seed_of(uint64_t tid, uint64_t seed) {
+  return (uint32_t)((tid + 1) * 0x9E3779B97F4A7C15ull >> 32) ^ (uint32_t)seed | 1u;
 }
 
 __global__ void k_l2(float* table, uint32_t cells, int per_thread, uint64_t seed) {
-  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t s = seed_of((uint64_t)blockIdx.x * blockDim.x + threadIdx.x, seed);
   for (int k = 0; k < per_thread; ++k) {
-    const uint64_t w = mix64(seed + tid * 0x9E3779B97F4A7C15ull + k);
-    atomicAdd(table + (uint32_t)(w % cells), (w >> 63) ? -1.f : 1.f);
+    const uint32_t r = xs32(s);
+    atomicAdd(table + cell_of(r, cells), (r & 1u) ? -1.f : 1.f);
   }
 }
 
@@ -36,10 +43,10 @@ __global__ void k_smem(float* out, uint32_t cells, int per_thread, uint64_t seed
   extern __shared__ float t[];
   for (uint32_t i = threadIdx.x; i < cells; i += blockDim.x) t[i] = 0.f;
   __syncthreads();
-  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t s = seed_of((uint64_t)blockIdx.x * blockDim.x + threadIdx.x, seed);
   for (int k = 0; k < per_thread; ++k) {
-    const uint64_t w = mix64(seed + tid * 0x9E3779B97F4A7C15ull + k);
-    atomicAdd(t + (uint32_t)(w % cells), (w >> 63) ? -1.f : 1.f);
+    const uint32_t r = xs32(s);
+    atomicAdd(t + cell_of(r, cells), (r & 1u) ? -1.f : 1.f);
   }
   __syncthreads();
   if (threadIdx.x == 0) out[blockIdx.x] = t[0];
@@ -51,13 +58,12 @@ __global__ void k_dsmem(float* out, uint32_t cells_per_cta, int per_thread, uint
   const uint32_t nrank = cl.num_blocks();
   for (uint32_t i = threadIdx.x; i < cells_per_cta; i += blockDim.x) t[i] = 0.f;
   cl.sync();
-  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint32_t cells = cells_per_cta * nrank;
+  uint32_t s = seed_of((uint64_t)blockIdx.x * blockDim.x + threadIdx.x, seed);
   for (int k = 0; k < per_thread; ++k) {
-    const uint64_t w = mix64(seed + tid * 0x9E3779B97F4A7C15ull + k);
-    const uint32_t c = (uint32_t)(w % cells);
-    float* dst = cl.map_shared_rank(t, c / cells_per_cta) + (c % cells_per_cta);
-    atomicAdd(dst, (w >> 63) ? -1.f : 1.f);  // remote (or local) shared-memory atomic over DSMEM
+    const uint32_t r = xs32(s);
+    const uint32_t rank = cell_of(r, nrank), c = cell_of(r * 2654435761u, cells_per_cta);
+    float* dst = cl.map_shared_rank(t, rank) + c;
+    atomicAdd(dst, (r & 1u) ? -1.f : 1.f);  // remote (or local) shared-memory atomic over DSMEM
   }
   cl.sync();
   if (threadIdx.x == 0) out[blockIdx.x] = t[0];
@@ -67,15 +73,12 @@ __global__ void k_dsmem(float* out, uint32_t cells_per_cta, int per_thread, uint
 // the access pattern of the decode's sketch queries (r gathers per union coordinate)
 template <int ILP>
 __global__ void k_gather(const float* __restrict__ table, uint32_t cells, int per_thread, uint64_t seed, float* out) {
-  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t s = seed_of((uint64_t)blockIdx.x * blockDim.x + threadIdx.x, seed);
   float acc = 0.f;
   for (int k = 0; k < per_thread; k += ILP) {
     float v[ILP];
 #pragma unroll
-    for (int u = 0; u < ILP; ++u) {
-      const uint64_t w = mix64(seed + tid * 0x9E3779B97F4A7C15ull + k + u);
-      v[u] = __ldg(table + (uint32_t)(w % cells));
-    }
+    for (int u = 0; u < ILP; ++u) v[u] = __ldg(table + cell_of(xs32(s), cells));
 #pragma unroll
     for (int u = 0; u < ILP; ++u) acc += v[u];
   }

@@ -41,7 +41,13 @@ def train(hook: bool, ef: bool = False, cap_mb: float = 1000):
     torch.manual_seed(0)
     model = Model().cuda()
     ddp = nn.parallel.DistributedDataParallel(model, device_ids=[rank], bucket_cap_mb=cap_mb)
-    state = S2HookState(size_ratio=4.0, alpha=0.3, seed=1, error_feedback=ef)
+    # With error feedback against the MERGED estimate (SPEC.md ef_step: e' = g~ - g^) every rank's
+    # residual also carries its disagreement with the average, which the sketch must then carry:
+    # a sketch sized for the raw gradient (alpha 0.3, lambda 4) diverges to Inf within ~100 steps
+    # (and the hook raises the reference's NaN/Inf ValueError).  EF runs get a sketch with 8 cells
+    # per coordinate.
+    state = (S2HookState(size_ratio=8.0, alpha=1.0, seed=1, error_feedback=True) if ef
+             else S2HookState(size_ratio=4.0, alpha=0.3, seed=1, error_feedback=False))
     if hook:
         ddp.register_comm_hook(state, diag_hook)
     opt = torch.optim.SGD(ddp.parameters(), lr=2.0)
