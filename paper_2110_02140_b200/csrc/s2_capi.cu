@@ -347,8 +347,11 @@ static int64_t layout_p2p(s2_plan* plan, int W, int G) {
   const int oneshot_maxw = os_env ? atoi(os_env) : 2;
   a.oneshot = (W <= oneshot_maxw && W <= 4) ? 1 : 0;
   for (int k = 0; k < 2; ++k) a.off_tsum[k] = a.oneshot ? take(cells * 4) : a.off_table[k];
+  // push (data stored into the peers' inboxes before each flag) is the default for the two-shot
+  // exchange: W = 4 step 84.9 -> 82.0 µs; the one-shot keeps pulling: W = 2 push 67.3 vs pull
+  // 66.1 µs (profiles/r02_push_ab.txt).  S2_P2P_PUSH=0/1 forces either.
   const char* pe = getenv("S2_P2P_PUSH");
-  a.push = pe ? atoi(pe) : 0;
+  a.push = pe ? atoi(pe) : (a.oneshot ? 0 : 1);
   // inbox: one-shot W slots of the whole table + bitmap, two-shot W slots of one slice each
   for (int k = 0; k < 2; ++k) a.off_inbox[k] = a.push ? take((a.oneshot ? W : 1) * (cells + words) * 4) : -1;
   a.cells = cells;

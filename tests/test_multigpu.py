@@ -18,11 +18,11 @@ def ngpus():
 
 
 VARIANTS = {
-    "ipc": {},                                 # default: CUDA-IPC arena, one-shot (W=2) / two-shot (W>2)
-    "ipc_twoshot": {"S2_P2P_ONESHOT_MAXW": "1"},
-    "ipc_oneshot": {"S2_P2P_ONESHOT_MAXW": "4"},
-    "push": {"S2_P2P_PUSH": "1"},              # data pushed into the peers' inboxes before each flag
-    "push_twoshot": {"S2_P2P_PUSH": "1", "S2_P2P_ONESHOT_MAXW": "1"},
+    "ipc": {},                                 # default: CUDA-IPC arena, pull one-shot (W=2) / push two-shot (W>2)
+    "ipc_twoshot": {"S2_P2P_ONESHOT_MAXW": "1"},   # push two-shot at W = 2 too
+    "ipc_oneshot": {"S2_P2P_ONESHOT_MAXW": "4"},   # pull one-shot at W = 4
+    "pull": {"S2_P2P_PUSH": "0", "S2_P2P_ONESHOT_MAXW": "1"},  # pull two-shot (peers read after the flag)
+    "push_oneshot": {"S2_P2P_PUSH": "1"},      # push one-shot
     "nccl": {"S2_AGG": "nccl"},                # NCCL all-reduce + all-gather + OR kernel (north-star literal)
     "graph": {"S2_CHECK_GRAPH": "1"},          # CUDA-graph replay of the whole reduce
     "blocks": {"S2_CHECK_NUM_BLOCKS": "62500"},  # block bitmap (b < d, 32 elements per block)

@@ -92,11 +92,10 @@ for name, ef, cap in (("s2", False, 1000), ("s2_ef_buckets", True, 0.03)):
     r = {"loss_last": float(np.mean(l_s2[-20:])), "loss_first": float(np.mean(l_s2[:10])),
          "max_rel_err": max(DIAG), "grads_replicated": len(set(h)) == 1, "bucket_sizes": len(state.reducers),
          "residuals": len(state.residuals)}
-    # without EF the estimate must track the exact average; with EF (residuals densify the
-    # compressed vector, DDP.py docstring) the run must still converge
-    r["ok"] = r["grads_replicated"] and (
-        (r["loss_last"] <= 1.1 * rep["loss_exact_last"] and r["max_rel_err"] < 0.1) if not ef
-        else r["loss_last"] < 0.5 * r["loss_first"])
+    # both runs must train as well as exact all-reduce; without EF the per-step estimate must also
+    # stay close to the exact average (with EF the hook's input carries the residual)
+    r["ok"] = (r["grads_replicated"] and r["loss_last"] <= 1.1 * rep["loss_exact_last"]
+               and r["loss_last"] < r["loss_first"] and (ef or r["max_rel_err"] < 0.1))
     rep[name] = r
     rep["ok"] &= r["ok"]
 if rank == 0:
