@@ -398,6 +398,9 @@ static int finish_p2p(s2_plan* plan, int G) {
     S2_CUDA(cudaMemset(plan->counters[k], 0, sizeof(unsigned long long) * S2_NUM_COUNTERS), "cudaMemset(counters)");
   }
   plan->phase = 0;
+  S2_CUDA(s2::preload_compress(plan->p), "preload compress");
+  S2_CUDA(s2::preload_decode(plan->p), "preload decode");
+  S2_CUDA(s2::preload_p2p(plan->pa), "preload exchange");
   S2_CUDA(cudaDeviceSynchronize(), "p2p init");
   return S2_OK;
 }

@@ -261,6 +261,16 @@ static cudaError_t launch_compress_r(const Plan& p, const float* g, uint32_t* bi
   return launch_compress_rk<R, kCompressKF>(p, g, bitmap, table, counters, mode, st);
 }
 
+cudaError_t preload_compress(const Plan& p) {
+  cudaFuncAttributes fa;
+  switch (p.hp.rows) {
+    case 1: return cudaFuncGetAttributes(&fa, k_compress<1, 0, kCompressKF>);
+    case 3: return cudaFuncGetAttributes(&fa, k_compress<3, 0, kCompressKF>);
+    case 5: return cudaFuncGetAttributes(&fa, k_compress<5, 0, kCompressKF>);
+    default: return cudaFuncGetAttributes(&fa, k_compress<0, 0, kCompressKF>);
+  }
+}
+
 cudaError_t launch_compress(const Plan& p, const float* g, uint32_t* bitmap, float* table,
                             unsigned long long* counters, int mode, cudaStream_t st, bool prezeroed) {
   cudaError_t e = cudaSuccess;

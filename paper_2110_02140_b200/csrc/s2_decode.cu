@@ -75,6 +75,18 @@ static cudaError_t launch_decode_r(const Plan& p, const uint32_t* bitmap, const 
                    pow2, out, z4, zn4, zc, p.hp, health);
 }
 
+cudaError_t preload_decode(const Plan& p) {
+  cudaFuncAttributes fa;
+  const bool blocks = p.block_size != 1;
+  switch (p.hp.rows) {
+#define S2_CASE(r) \
+  case r: return cudaFuncGetAttributes(&fa, blocks ? k_decode<r, true> : k_decode<r, false>);
+    S2_CASE(1) S2_CASE(2) S2_CASE(3) S2_CASE(4) S2_CASE(5)
+#undef S2_CASE
+    default: return cudaFuncGetAttributes(&fa, blocks ? k_decode<0, true> : k_decode<0, false>);
+  }
+}
+
 cudaError_t launch_decode(const Plan& p, const uint32_t* bitmap, const float* table, int workers,
                           float* out, cudaStream_t st, float* zero_table, unsigned long long* zero_counters,
                           const DecodeHealth* health) {

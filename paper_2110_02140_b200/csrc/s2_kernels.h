@@ -71,4 +71,12 @@ struct P2PArgs {
 };
 cudaError_t launch_p2p_aggregate(const P2PArgs& a, int grid, cudaStream_t st);
 
+// Load the kernels a peer-memory plan will launch (cudaFuncGetAttributes forces CUDA's lazy module
+// loading now).  A lazy load inside a launch can wait for running kernels; when one host thread
+// drives several ranks (the single-GPU harness) that wait would hold back the launches the
+// spinning exchange is waiting for.
+cudaError_t preload_compress(const Plan& p);
+cudaError_t preload_decode(const Plan& p);
+cudaError_t preload_p2p(const P2PArgs& a);
+
 }  // namespace s2

@@ -391,41 +391,18 @@ __global__ void __launch_bounds__(kP2PThreads) k_p2p_push_twoshot(const __grid_c
   S2_TRACE(4);
 }
 
+static const void* p2p_kernel(const P2PArgs& a);
+
+cudaError_t preload_p2p(const P2PArgs& a) {
+  const void* fn = p2p_kernel(a);
+  if (fn == nullptr) return cudaErrorInvalidValue;
+  cudaFuncAttributes fa;
+  return cudaFuncGetAttributes(&fa, fn);
+}
+
 cudaError_t launch_p2p_aggregate(const P2PArgs& a, int grid, cudaStream_t st) {
-  const void* fn = nullptr;
-  if (a.push) {
-    switch (a.world * 2 + a.oneshot) {
-      case 5: fn = (const void*)k_p2p_push_oneshot<2>; break;
-      case 7: fn = (const void*)k_p2p_push_oneshot<3>; break;
-      case 9: fn = (const void*)k_p2p_push_oneshot<4>; break;
-      case 4: fn = (const void*)k_p2p_push_twoshot<2>; break;
-      case 6: fn = (const void*)k_p2p_push_twoshot<3>; break;
-      case 8: fn = (const void*)k_p2p_push_twoshot<4>; break;
-      case 10: fn = (const void*)k_p2p_push_twoshot<5>; break;
-      case 12: fn = (const void*)k_p2p_push_twoshot<6>; break;
-      case 14: fn = (const void*)k_p2p_push_twoshot<7>; break;
-      case 16: fn = (const void*)k_p2p_push_twoshot<8>; break;
-      default: return cudaErrorInvalidValue;
-    }
-  } else if (a.oneshot) {
-    switch (a.world) {
-      case 2: fn = (const void*)k_p2p_oneshot<2>; break;
-      case 3: fn = (const void*)k_p2p_oneshot<3>; break;
-      case 4: fn = (const void*)k_p2p_oneshot<4>; break;
-      default: return cudaErrorInvalidValue;
-    }
-  } else {
-    switch (a.world) {
-      case 2: fn = (const void*)k_p2p_aggregate<2>; break;
-      case 3: fn = (const void*)k_p2p_aggregate<3>; break;
-      case 4: fn = (const void*)k_p2p_aggregate<4>; break;
-      case 5: fn = (const void*)k_p2p_aggregate<5>; break;
-      case 6: fn = (const void*)k_p2p_aggregate<6>; break;
-      case 7: fn = (const void*)k_p2p_aggregate<7>; break;
-      case 8: fn = (const void*)k_p2p_aggregate<8>; break;
-      default: return cudaErrorInvalidValue;
-    }
-  }
+  const void* fn = p2p_kernel(a);
+  if (fn == nullptr) return cudaErrorInvalidValue;
   // Plain programmatic launch: CTAs only wait on the same CTA index of the other ranks
   // (measured 1.7 µs per step faster at W = 2 and 4 than a cooperative launch).
   cudaLaunchConfig_t cfg = {};
@@ -440,6 +417,44 @@ cudaError_t launch_p2p_aggregate(const P2PArgs& a, int grid, cudaStream_t st) {
   cfg.numAttrs = 1;
   void* args[] = {const_cast<P2PArgs*>(&a)};
   return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
+static const void* p2p_kernel(const P2PArgs& a) {
+  const void* fn = nullptr;
+  if (a.push) {
+    switch (a.world * 2 + a.oneshot) {
+      case 5: fn = (const void*)k_p2p_push_oneshot<2>; break;
+      case 7: fn = (const void*)k_p2p_push_oneshot<3>; break;
+      case 9: fn = (const void*)k_p2p_push_oneshot<4>; break;
+      case 4: fn = (const void*)k_p2p_push_twoshot<2>; break;
+      case 6: fn = (const void*)k_p2p_push_twoshot<3>; break;
+      case 8: fn = (const void*)k_p2p_push_twoshot<4>; break;
+      case 10: fn = (const void*)k_p2p_push_twoshot<5>; break;
+      case 12: fn = (const void*)k_p2p_push_twoshot<6>; break;
+      case 14: fn = (const void*)k_p2p_push_twoshot<7>; break;
+      case 16: fn = (const void*)k_p2p_push_twoshot<8>; break;
+      default: return nullptr;
+    }
+  } else if (a.oneshot) {
+    switch (a.world) {
+      case 2: fn = (const void*)k_p2p_oneshot<2>; break;
+      case 3: fn = (const void*)k_p2p_oneshot<3>; break;
+      case 4: fn = (const void*)k_p2p_oneshot<4>; break;
+      default: return nullptr;
+    }
+  } else {
+    switch (a.world) {
+      case 2: fn = (const void*)k_p2p_aggregate<2>; break;
+      case 3: fn = (const void*)k_p2p_aggregate<3>; break;
+      case 4: fn = (const void*)k_p2p_aggregate<4>; break;
+      case 5: fn = (const void*)k_p2p_aggregate<5>; break;
+      case 6: fn = (const void*)k_p2p_aggregate<6>; break;
+      case 7: fn = (const void*)k_p2p_aggregate<7>; break;
+      case 8: fn = (const void*)k_p2p_aggregate<8>; break;
+      default: return nullptr;
+    }
+  }
+  return fn;
 }
 
 }  // namespace s2
