@@ -162,9 +162,11 @@ int s2_aggregate(s2_plan* plan, float* table, const uint32_t* bitmap, uint32_t* 
                  void* stream);
 /* the whole reduce: compress -> aggregate -> decode (÷ world) using plan-owned
  * scratch; out = float32[dim] averaged gradient.  counters may be NULL (then the
- * plan's own are used, see s2_last_counters).  Plan-owned sketch tables and
- * counters alternate between consecutive calls (the decode of call i zeroes the
- * buffers of call i+1), so a CUDA graph must capture an even number of calls. */
+ * plan's own are used, see s2_last_counters).  Plan-owned buffers rotate with period 4
+ * (call i uses table / counters slot i % 4 and bitmap slot i % 2; its decode zeroes slot
+ * (i+2) % 4), so a CUDA graph must capture a multiple of 4 calls.  The compress of call i+1
+ * shares no buffer with the decode of call i and overlaps it through programmatic dependent
+ * launch, unless g aliases the previous call's out (then it waits; S2_OVERLAP=0 disables). */
 int s2_reduce(s2_plan* plan, const float* g, float* out, uint64_t* counters, void* stream);
 /* every later s2_reduce's decode writes its S2_STATUS_* bits (0 = healthy) into *status
  * (device memory or mapped pinned host memory; NULL disables) — lets a caller check the

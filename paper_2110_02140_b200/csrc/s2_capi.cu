@@ -22,13 +22,17 @@ struct s2_plan {
   int world = 1;
   int rank = 0;
   ncclComm_t comm = nullptr;
-  // plan-owned scratch for s2_reduce / s2_aggregate.  Sketch tables and counters
-  // ping-pong: the decode of reduce i zeroes the buffers reduce i+1 compresses into,
-  // so the hot path has no memset launches.
-  float* tables[2] = {nullptr, nullptr};
-  unsigned long long* counters[2] = {nullptr, nullptr};
-  int phase = 0;
-  uint32_t* bitmap = nullptr;
+  // plan-owned scratch for s2_reduce / s2_aggregate.  Reduce i uses sketch table and counters
+  // slot i % 4 and bitmap slot i % 2; its decode zeroes table / counters slot (i + 2) % 4, so the
+  // hot path has no memset launches and the compress of reduce i+1 (slots (i+1) % 4, (i+1) % 2)
+  // shares no buffer with the decode of reduce i and may overlap it (late_wait).
+  static constexpr int kTableSlots = 4;
+  float* tables[kTableSlots] = {};
+  unsigned long long* counters[kTableSlots] = {};
+  uint64_t step = 0;
+  uint32_t* bitmaps[2] = {nullptr, nullptr};
+  const float* prev_out = nullptr;  // the previous reduce's output (alias check for late_wait)
+  int overlap = -1;                 // S2_OVERLAP (default 1)
   uint32_t* unionmap = nullptr;
   uint32_t* gather = nullptr;  // world * words (all-gather landing buffer)
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // optional phase timing events
@@ -173,16 +177,19 @@ int s2_plan_create(int64_t dim, int64_t num_blocks, int rows, int64_t cols, uint
 }
 
 static void free_scratch(s2_plan* p) {
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < s2_plan::kTableSlots; ++k) {
     if (!p->p2p) cudaFree(p->tables[k]);
     cudaFree(p->counters[k]);
     p->tables[k] = nullptr;
     p->counters[k] = nullptr;
   }
-  cudaFree(p->bitmap);
+  for (int k = 0; k < 2; ++k) {
+    cudaFree(p->bitmaps[k]);
+    p->bitmaps[k] = nullptr;
+  }
   cudaFree(p->unionmap);
   cudaFree(p->gather);
-  p->bitmap = p->unionmap = p->gather = nullptr;
+  p->unionmap = p->gather = nullptr;
 }
 
 static void free_p2p(s2_plan* p) {
@@ -192,8 +199,8 @@ static void free_p2p(s2_plan* p) {
   if (p->arena && p->arena_owned) cudaFree(p->arena);
   p->arena = nullptr;
   p->arena_owned = false;
-  if (p->p2p) {  // tables/counters pointed into the arena / were separately allocated
-    p->tables[0] = p->tables[1] = nullptr;
+  if (p->p2p) {  // tables pointed into the arena
+    for (int k = 0; k < s2_plan::kTableSlots; ++k) p->tables[k] = nullptr;
   }
   p->p2p = false;
 }
@@ -305,14 +312,14 @@ static int ensure_scratch(s2_plan* p) {
   if (p->tables[0] || p->p2p) return S2_OK;
   const size_t cells4 = ((size_t)p->p.hp.rows * p->p.hp.cols + 3) / 4 * 4;  // decode zeroes float4s
   const size_t wb = sizeof(uint32_t) * ((size_t)p->p.words + 4);
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < s2_plan::kTableSlots; ++k) {
     S2_CUDA(cudaMalloc(&p->tables[k], cells4 * sizeof(float)), "cudaMalloc(table)");
     S2_CUDA(cudaMemset(p->tables[k], 0, cells4 * sizeof(float)), "cudaMemset(table)");
     S2_CUDA(cudaMalloc(&p->counters[k], sizeof(unsigned long long) * S2_NUM_COUNTERS), "cudaMalloc(counters)");
     S2_CUDA(cudaMemset(p->counters[k], 0, sizeof(unsigned long long) * S2_NUM_COUNTERS), "cudaMemset(counters)");
   }
-  p->phase = 0;
-  S2_CUDA(cudaMalloc(&p->bitmap, wb), "cudaMalloc(bitmap)");
+  p->step = 0;
+  for (int k = 0; k < 2; ++k) S2_CUDA(cudaMalloc(&p->bitmaps[k], wb), "cudaMalloc(bitmap)");
   S2_CUDA(cudaMalloc(&p->unionmap, wb), "cudaMalloc(union)");
   if (p->world > 1)
     S2_CUDA(cudaMalloc(&p->gather, sizeof(uint32_t) * (size_t)p->p.words * p->world), "cudaMalloc(gather)");
@@ -323,7 +330,7 @@ static int ensure_scratch(s2_plan* p) {
 static int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 // Arena layout (identical on every rank):
-//   tables[2] | bitmaps[2] | unions[2] | flags_a[W*8G] | flags_b[W*8G] | epochs[8G] | error | tsum[2]?
+//   tables[4] | bitmaps[2] | unions[2] | flags_a[W*8G] | flags_b[W*8G] | epochs[8G] | error | tsum[2]?
 //   | inbox[2]? (push exchange)
 // (flag and epoch slots for exchange grids of up to 8 CTAs per SM)
 static int64_t layout_p2p(s2_plan* plan, int W, int G) {
@@ -336,7 +343,7 @@ static int64_t layout_p2p(s2_plan* plan, int W, int G) {
     off = round_up(off + bytes, 256);
     return o;
   };
-  for (int k = 0; k < 2; ++k) a.off_table[k] = take(cells * 4);
+  for (int k = 0; k < s2_plan::kTableSlots; ++k) a.off_table[k] = take(cells * 4);
   for (int k = 0; k < 2; ++k) a.off_bitmap[k] = take(words * 4);
   for (int k = 0; k < 2; ++k) a.off_union[k] = take(words * 4);
   a.off_flags_a = take((int64_t)W * 8 * G * 4);
@@ -346,7 +353,7 @@ static int64_t layout_p2p(s2_plan* plan, int W, int G) {
   const char* os_env = getenv("S2_P2P_ONESHOT_MAXW");
   const int oneshot_maxw = os_env ? atoi(os_env) : 2;
   a.oneshot = (W <= oneshot_maxw && W <= 4) ? 1 : 0;
-  for (int k = 0; k < 2; ++k) a.off_tsum[k] = a.oneshot ? take(cells * 4) : a.off_table[k];
+  for (int k = 0; k < 2; ++k) a.off_tsum[k] = a.oneshot ? take(cells * 4) : -1;  // two-shot: in place
   // push (data stored into the peers' inboxes before each flag) is the default for the two-shot
   // exchange: W = 4 step 84.9 -> 82.0 µs; the one-shot keeps pulling: W = 2 push 67.3 vs pull
   // 66.1 µs (profiles/r02_push_ab.txt).  S2_P2P_PUSH=0/1 forces either.
@@ -392,12 +399,12 @@ static int finish_p2p(s2_plan* plan, int G) {
     S2_CUDA(cudaMalloc(&a.trace, sizeof(unsigned long long) * 64 * G), "cudaMalloc(trace)");
     S2_CUDA(cudaMemset(a.trace, 0, sizeof(unsigned long long) * 64 * G), "cudaMemset(trace)");
   }
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < s2_plan::kTableSlots; ++k) {
     plan->tables[k] = reinterpret_cast<float*>(plan->arena + a.off_table[k]);
     S2_CUDA(cudaMalloc(&plan->counters[k], sizeof(unsigned long long) * S2_NUM_COUNTERS), "cudaMalloc(counters)");
     S2_CUDA(cudaMemset(plan->counters[k], 0, sizeof(unsigned long long) * S2_NUM_COUNTERS), "cudaMemset(counters)");
   }
-  plan->phase = 0;
+  plan->step = 0;
   S2_CUDA(s2::preload_compress(plan->p), "preload compress");
   S2_CUDA(s2::preload_decode(plan->p), "preload decode");
   S2_CUDA(s2::preload_p2p(plan->pa), "preload exchange");
@@ -606,13 +613,24 @@ int s2_reduce(s2_plan* plan, const float* g, float* out, uint64_t* counters, voi
   int rc = ensure_scratch(plan);
   if (rc) return rc;
   cudaStream_t st = as_stream(stream);
-  const int cur = plan->phase, nxt = cur ^ 1;
-  float* table = plan->tables[cur];
-  uint32_t* bitmap = plan->p2p ? reinterpret_cast<uint32_t*>(plan->arena + plan->pa.off_bitmap[cur]) : plan->bitmap;
-  // caller counters: zeroed by memset; plan counters: zeroed by the previous decode
-  unsigned long long* cnt = counters ? reinterpret_cast<unsigned long long*>(counters) : plan->counters[cur];
+  const int cur = (int)(plan->step & 1), tc = (int)(plan->step & 3), tz = (int)((plan->step + 2) & 3);
+  float* table = plan->tables[tc];
+  uint32_t* bitmap = plan->p2p ? reinterpret_cast<uint32_t*>(plan->arena + plan->pa.off_bitmap[cur]) : plan->bitmaps[cur];
+  // caller counters: zeroed by memset; plan counters: zeroed by the decode two reduces back
+  unsigned long long* cnt = counters ? reinterpret_cast<unsigned long long*>(counters) : plan->counters[tc];
+  // The compress may overlap the previous reduce's decode (it shares no buffer with it) unless its
+  // input is that decode's output (g aliasing the previous out) — then it waits up front.
+  if (plan->overlap < 0) {
+    const char* e = getenv("S2_OVERLAP");
+    plan->overlap = e ? atoi(e) : 1;
+  }
+  const size_t nb = sizeof(float) * (size_t)plan->p.dim;
+  const char* gb = reinterpret_cast<const char*>(g);
+  const char* pb = reinterpret_cast<const char*>(plan->prev_out);
+  const bool alias = pb != nullptr && gb < pb + nb && pb < gb + nb;
+  const bool late = plan->overlap != 0 && !alias;
   if (plan->ev[0]) cudaEventRecord(plan->ev[0], st);
-  S2_CUDA(s2::launch_compress(plan->p, g, bitmap, table, cnt, S2_MASK_NONZERO, st, counters == nullptr),
+  S2_CUDA(s2::launch_compress(plan->p, g, bitmap, table, cnt, S2_MASK_NONZERO, st, counters == nullptr, late),
           "s2_reduce/compress");
   if (plan->ev[1]) cudaEventRecord(plan->ev[1], st);
   const uint32_t* un = bitmap;
@@ -620,9 +638,10 @@ int s2_reduce(s2_plan* plan, const float* g, float* out, uint64_t* counters, voi
   if (plan->world > 1) {
     if (plan->p2p) {
       plan->pa.cur = cur;
+      plan->pa.tcur = tc;
       S2_CUDA(s2::launch_p2p_aggregate(plan->pa, plan->p2p_grid, st), "s2_reduce/p2p aggregate");
       un = reinterpret_cast<const uint32_t*>(plan->arena + plan->pa.off_union[cur]);
-      table = reinterpret_cast<float*>(plan->arena + plan->pa.off_tsum[cur]);  // two-shot: tables[cur] in place
+      if (plan->pa.oneshot) table = reinterpret_cast<float*>(plan->arena + plan->pa.off_tsum[cur]);  // else in place
       health.poison = reinterpret_cast<const uint32_t*>(plan->arena + plan->pa.off_error);
     } else {
       rc = s2_aggregate(plan, table, bitmap, plan->unionmap, stream);
@@ -631,10 +650,11 @@ int s2_reduce(s2_plan* plan, const float* g, float* out, uint64_t* counters, voi
     }
   }
   if (plan->ev[2]) cudaEventRecord(plan->ev[2], st);
-  S2_CUDA(s2::launch_decode(plan->p, un, table, plan->world, out, st, plan->tables[nxt], plan->counters[nxt], &health),
+  S2_CUDA(s2::launch_decode(plan->p, un, table, plan->world, out, st, plan->tables[tz], plan->counters[tz], &health),
           "s2_reduce/decode");
   if (plan->ev[3]) cudaEventRecord(plan->ev[3], st);
-  plan->phase = nxt;
+  plan->prev_out = out;
+  plan->step += 1;
   return S2_OK;
 }
 
@@ -672,7 +692,7 @@ int s2_read_counters(const s2_plan* plan, uint64_t* host_out, void* stream) {
     return S2_OK;
   }
   cudaStream_t st = as_stream(stream);
-  S2_CUDA(cudaMemcpyAsync(host_out, plan->counters[plan->phase ^ 1], sizeof(uint64_t) * S2_NUM_COUNTERS,
+  S2_CUDA(cudaMemcpyAsync(host_out, plan->counters[(plan->step + 3) & 3], sizeof(uint64_t) * S2_NUM_COUNTERS,
                           cudaMemcpyDeviceToHost, st), "read counters");
   S2_CUDA(cudaStreamSynchronize(st), "read counters");
   return S2_OK;
@@ -680,7 +700,7 @@ int s2_read_counters(const s2_plan* plan, uint64_t* host_out, void* stream) {
 
 const uint64_t* s2_last_counters(const s2_plan* plan) {
   if (!plan || !plan->counters[0]) return nullptr;
-  return reinterpret_cast<const uint64_t*>(plan->counters[plan->phase ^ 1]);
+  return reinterpret_cast<const uint64_t*>(plan->counters[(plan->step + 3) & 3]);
 }
 
 }  // extern "C"

@@ -66,7 +66,7 @@ template <int R, int MODE, int KF>
 __global__ void __launch_bounds__(kThreads, 2)
 k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __restrict__ bitmap,
            float* __restrict__ table, unsigned long long* __restrict__ counters,
-           const __grid_constant__ HashParams hp) {
+           const __grid_constant__ HashParams hp, int late_wait) {
   constexpr int kT = 128 * KF;  // elements per warp tile
   constexpr int kW = 4 * KF;    // bitmap words per warp tile
   constexpr int kCap = 32 + kQFast;
@@ -89,7 +89,7 @@ k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __res
   uint32_t bad = 0;
   float fin = 0.f;  // MODE 2: sum of 0*x, NaN iff a non-finite element was seen
 
-  griddep_wait();  // g may be written by the caller's previous kernel
+  if (!late_wait) griddep_wait();  // g may be written by the caller's previous kernel
   griddep_launch_dependents();
   int64_t t = (int64_t)blockIdx.x * kWarps + wib;
   float4 vn[KF];
@@ -223,6 +223,7 @@ k_compress(const float* __restrict__ g, int64_t dim, int64_t bs, uint32_t* __res
     if (MODE == 2 && sel) atomicAdd(counters + S2_CNT_SELECTED, sel);
     if (bad) atomicOr(counters + S2_CNT_NONFINITE, 1ull);
   }
+  if (late_wait) griddep_wait();  // complete only after the stream predecessor (see launch_compress)
 }
 
 // =================================================================== launchers
@@ -237,7 +238,7 @@ constexpr int kCompressKF = 8;
 
 template <int R, int KF>
 static cudaError_t launch_compress_rk(const Plan& p, const float* g, uint32_t* bitmap, float* table,
-                                      unsigned long long* counters, int mode, cudaStream_t st) {
+                                      unsigned long long* counters, int mode, cudaStream_t st, int late) {
   const int64_t ntiles = (p.dim + 128 * KF - 1) / (128 * KF);
   static int per_sm = -1;  // S2_COMPRESS_CTAS_PER_SM: grid = SMs x this (> resident -> extra waves)
   if (per_sm < 0) {
@@ -247,18 +248,18 @@ static cudaError_t launch_compress_rk(const Plan& p, const float* g, uint32_t* b
   const int grid = grid_for(ntiles, per_sm > 0 ? per_sm : 2);
   if (mode == S2_MASK_GIVEN)
     return launch_ex(k_compress<R, 2, KF>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table, counters,
-                     p.hp);
+                     p.hp, late);
   if (p.block_size == 1)
     return launch_ex(k_compress<R, 0, KF>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table, counters,
-                     p.hp);
+                     p.hp, late);
   return launch_ex(k_compress<R, 1, KF>, grid, kThreads, 0, st, g, p.dim, p.block_size, bitmap, table, counters,
-                   p.hp);
+                   p.hp, late);
 }
 
 template <int R>
 static cudaError_t launch_compress_r(const Plan& p, const float* g, uint32_t* bitmap, float* table,
-                                     unsigned long long* counters, int mode, cudaStream_t st) {
-  return launch_compress_rk<R, kCompressKF>(p, g, bitmap, table, counters, mode, st);
+                                     unsigned long long* counters, int mode, cudaStream_t st, int late) {
+  return launch_compress_rk<R, kCompressKF>(p, g, bitmap, table, counters, mode, st, late);
 }
 
 cudaError_t preload_compress(const Plan& p) {
@@ -272,7 +273,8 @@ cudaError_t preload_compress(const Plan& p) {
 }
 
 cudaError_t launch_compress(const Plan& p, const float* g, uint32_t* bitmap, float* table,
-                            unsigned long long* counters, int mode, cudaStream_t st, bool prezeroed) {
+                            unsigned long long* counters, int mode, cudaStream_t st, bool prezeroed, bool late_wait) {
+  const int late = late_wait && prezeroed ? 1 : 0;  // memsets in between break the programmatic edge anyway
   cudaError_t e = cudaSuccess;
   if (!prezeroed) {
     e = cudaMemsetAsync(table, 0, sizeof(float) * (size_t)p.hp.rows * p.hp.cols, st);
@@ -285,10 +287,10 @@ cudaError_t launch_compress(const Plan& p, const float* g, uint32_t* bitmap, flo
     if (e != cudaSuccess) return e;
   }
   switch (p.hp.rows) {
-    case 1: e = launch_compress_r<1>(p, g, bitmap, table, counters, mode, st); break;
-    case 3: e = launch_compress_r<3>(p, g, bitmap, table, counters, mode, st); break;
-    case 5: e = launch_compress_r<5>(p, g, bitmap, table, counters, mode, st); break;
-    default: e = launch_compress_r<0>(p, g, bitmap, table, counters, mode, st); break;
+    case 1: e = launch_compress_r<1>(p, g, bitmap, table, counters, mode, st, late); break;
+    case 3: e = launch_compress_r<3>(p, g, bitmap, table, counters, mode, st, late); break;
+    case 5: e = launch_compress_r<5>(p, g, bitmap, table, counters, mode, st, late); break;
+    default: e = launch_compress_r<0>(p, g, bitmap, table, counters, mode, st, late); break;
   }
   if (e != cudaSuccess) return e;
   if (mode == S2_MASK_NONZERO && p.block_size > 1) return launch_selected_count(p, bitmap, counters, st);

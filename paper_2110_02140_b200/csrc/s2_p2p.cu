@@ -135,14 +135,14 @@ __device__ __forceinline__ uint4 or4(uint4 s, uint4 v) { return make_uint4(s.x |
 // index i < t4 is table vector i, else bitmap vector i - t4 (per-slice indexing).
 template <int W>
 __device__ __forceinline__ void reduce_batch(const P2PArgs& a, int64_t i0, int64_t hi, int64_t t4, int64_t w4) {
-  const int me = a.rank, cur = a.cur;
+  const int me = a.rank, cur = a.cur, tc = a.tcur;
   constexpr int B = p2p_batch<W>();
   uint4 v[B][W];
 #pragma unroll
   for (int k = 0; k < B; ++k) {
     const int64_t i = i0 + (int64_t)k * kP2PThreads;
     if (i < hi) {
-      const int64_t off = i < t4 ? a.off_table[cur] + (me * t4 + i) * 16 : a.off_bitmap[cur] + (me * w4 + i - t4) * 16;
+      const int64_t off = i < t4 ? a.off_table[tc] + (me * t4 + i) * 16 : a.off_bitmap[cur] + (me * w4 + i - t4) * 16;
 #pragma unroll
       for (int q = 0; q < W; ++q) v[k][q] = __ldcg(reinterpret_cast<const uint4*>(a.base[q] + off));
     }
@@ -155,7 +155,7 @@ __device__ __forceinline__ void reduce_batch(const P2PArgs& a, int64_t i0, int64
     if (i < t4) {  // sketch.merge: fixed rank order 0..W-1 -> identical sums on every rank
 #pragma unroll
       for (int q = 1; q < W; ++q) s = add4(s, v[k][q]);
-      *reinterpret_cast<uint4*>(a.base[me] + a.off_table[cur] + (me * t4 + i) * 16) = s;
+      *reinterpret_cast<uint4*>(a.base[me] + a.off_table[tc] + (me * t4 + i) * 16) = s;
     } else {  // BlockMask.union
 #pragma unroll
       for (int q = 1; q < W; ++q) s = or4(s, v[k][q]);
@@ -166,7 +166,7 @@ __device__ __forceinline__ void reduce_batch(const P2PArgs& a, int64_t i0, int64
 
 template <int W>
 __device__ __forceinline__ void gather_batch(const P2PArgs& a, int64_t i0, int64_t hi, int64_t t4, int64_t w4) {
-  const int me = a.rank, cur = a.cur;
+  const int me = a.rank, cur = a.cur, tc = a.tcur;
   constexpr int B = p2p_batch<W>();
   uint4 v[B][W];
 #pragma unroll
@@ -176,7 +176,7 @@ __device__ __forceinline__ void gather_batch(const P2PArgs& a, int64_t i0, int64
 #pragma unroll
       for (int q = 0; q < W; ++q) {
         if (q == me) continue;
-        const int64_t off = i < t4 ? a.off_table[cur] + (q * t4 + i) * 16 : a.off_union[cur] + (q * w4 + i - t4) * 16;
+        const int64_t off = i < t4 ? a.off_table[tc] + (q * t4 + i) * 16 : a.off_union[cur] + (q * w4 + i - t4) * 16;
         v[k][q] = __ldcg(reinterpret_cast<const uint4*>(a.base[q] + off));
       }
     }
@@ -188,7 +188,7 @@ __device__ __forceinline__ void gather_batch(const P2PArgs& a, int64_t i0, int64
 #pragma unroll
     for (int q = 0; q < W; ++q) {
       if (q == me) continue;
-      const int64_t off = i < t4 ? a.off_table[cur] + (q * t4 + i) * 16 : a.off_union[cur] + (q * w4 + i - t4) * 16;
+      const int64_t off = i < t4 ? a.off_table[tc] + (q * t4 + i) * 16 : a.off_union[cur] + (q * w4 + i - t4) * 16;
       *reinterpret_cast<uint4*>(a.base[me] + off) = v[k][q];
     }
   }
@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(kP2PThreads) k_p2p_oneshot(const __grid_consta
   asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic launch: compress must be complete
   S2_TRACE(0);
   const uint32_t ep = next_epoch(a, &s_ep);
-  const int me = a.rank, cur = a.cur;
+  const int me = a.rank, cur = a.cur, tc = a.tcur;
   const int64_t t4 = a.cells / 4, w4 = a.words / 4;
   int64_t lo, hi;
   chunk_of(t4 + w4, lo, hi);
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(kP2PThreads) k_p2p_oneshot(const __grid_consta
     for (int k = 0; k < B; ++k) {
       const int64_t i = i0 + (int64_t)k * kP2PThreads;
       if (i < hi) {
-        const int64_t off = i < t4 ? a.off_table[cur] + i * 16 : a.off_bitmap[cur] + (i - t4) * 16;
+        const int64_t off = i < t4 ? a.off_table[tc] + i * 16 : a.off_bitmap[cur] + (i - t4) * 16;
 #pragma unroll
         for (int q = 0; q < W; ++q) v[k][q] = __ldcg(reinterpret_cast<const uint4*>(a.base[q] + off));
       }
@@ -282,13 +282,13 @@ __global__ void __launch_bounds__(kP2PThreads) k_p2p_push_oneshot(const __grid_c
   asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic launch: compress must be complete
   S2_TRACE(0);
   const uint32_t ep = next_epoch(a, &s_ep);
-  const int me = a.rank, cur = a.cur;
+  const int me = a.rank, cur = a.cur, tc = a.tcur;
   const int64_t t4 = a.cells / 4, w4 = a.words / 4, slot = (t4 + w4) * 16;
   int64_t lo, hi;
   chunk_of(t4 + w4, lo, hi);
   const int64_t in_me = a.off_inbox[cur] + me * slot;
   for (int64_t i = lo + threadIdx.x; i < hi; i += kP2PThreads) {
-    const int64_t off = i < t4 ? a.off_table[cur] + i * 16 : a.off_bitmap[cur] + (i - t4) * 16;
+    const int64_t off = i < t4 ? a.off_table[tc] + i * 16 : a.off_bitmap[cur] + (i - t4) * 16;
     const uint4 v = __ldcg(reinterpret_cast<const uint4*>(a.base[me] + off));
 #pragma unroll
     for (int q = 0; q < W; ++q)
@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(kP2PThreads) k_p2p_push_oneshot(const __grid_c
     for (int k = 0; k < B; ++k) {
       const int64_t i = i0 + (int64_t)k * kP2PThreads;
       if (i < hi) {
-        const int64_t own = i < t4 ? a.off_table[cur] + i * 16 : a.off_bitmap[cur] + (i - t4) * 16;
+        const int64_t own = i < t4 ? a.off_table[tc] + i * 16 : a.off_bitmap[cur] + (i - t4) * 16;
 #pragma unroll
         for (int q = 0; q < W; ++q)
           v[k][q] = __ldcg(reinterpret_cast<const uint4*>(
@@ -339,14 +339,14 @@ __global__ void __launch_bounds__(kP2PThreads) k_p2p_push_twoshot(const __grid_c
   asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic launch: compress must be complete
   S2_TRACE(0);
   const uint32_t ep = next_epoch(a, &s_ep);
-  const int me = a.rank, cur = a.cur;
+  const int me = a.rank, cur = a.cur, tc = a.tcur;
   const int64_t t4 = a.cells / 4 / W, w4 = a.words / 4 / W, slot = (t4 + w4) * 16;  // per slice
   int64_t lo, hi;
   chunk_of(t4 + w4, lo, hi);
   // vector i of slice s in this rank's table / bitmap (local) and union
-  auto src = [&](int sl, int64_t i) { return i < t4 ? a.off_table[cur] + (sl * t4 + i) * 16
+  auto src = [&](int sl, int64_t i) { return i < t4 ? a.off_table[tc] + (sl * t4 + i) * 16
                                                     : a.off_bitmap[cur] + (sl * w4 + i - t4) * 16; };
-  auto dst = [&](int sl, int64_t i) { return i < t4 ? a.off_table[cur] + (sl * t4 + i) * 16
+  auto dst = [&](int sl, int64_t i) { return i < t4 ? a.off_table[tc] + (sl * t4 + i) * 16
                                                     : a.off_union[cur] + (sl * w4 + i - t4) * 16; };
   // reduce-scatter, push: slice q of my chunk -> inbox slot [me] of rank q
   for (int64_t i = lo + threadIdx.x; i < hi; i += kP2PThreads) {

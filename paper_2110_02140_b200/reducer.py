@@ -233,10 +233,10 @@ class HostPipeline:
 class GraphedReduce:
     """CUDA-graph replay of ``S2Reducer.reduce`` on static buffers (no per-step launch cost).
 
-    The plan's sketch tables and counters ping-pong between consecutive reduces, so two
-    graphs are captured — one per phase — and ``__call__`` replays the one matching the
-    plan's current phase.  Do not interleave direct ``reduce`` calls on the same reducer
-    with replays (they flip the phase too; an even number of them is harmless).
+    The plan rotates its buffers with period 4 (sketch tables / counters over 4 slots, bitmaps
+    over 2, s2_reduce), so four graphs are captured — one per slot — and ``__call__`` replays
+    them in order.  Do not interleave direct ``reduce`` calls on the same reducer with replays
+    (they advance the rotation too; a multiple of four of them is harmless).
 
         gr = GraphedReduce(reducer, g_static, out_static)
         g_static.copy_(grad); gr(); use(out_static)
@@ -247,15 +247,15 @@ class GraphedReduce:
         s = torch.cuda.Stream(device=reducer.device)
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
-            for _ in range(2):  # warm-up: scratch allocated, both phases exercised
+            for _ in range(4):  # warm-up: scratch allocated, every slot exercised
                 reducer.reduce(g_static, out=out_static, stream=s)
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
         reducer.check()
         self.graphs = []
         # each graph writes its health word into its own pinned slot (captured pointer)
-        self.words = torch.zeros(2, dtype=torch.int32, pin_memory=True)
-        for k in range(2):
+        self.words = torch.zeros(4, dtype=torch.int32, pin_memory=True)
+        for k in range(4):
             check(lib.s2_plan_set_status(reducer.plan.handle, ctypes.c_void_p(self.words.data_ptr() + 4 * k)),
                   "set status")
             gph = torch.cuda.CUDAGraph()
@@ -264,9 +264,9 @@ class GraphedReduce:
                       "reduce")
             self.graphs.append(gph)
         check(lib.s2_plan_set_status(reducer.plan.handle, None), "set status")
-        # capture flipped the phase twice: back at the phase graph 0 was recorded in
+        # capture advanced the rotation by four: back at the slot graph 0 was recorded in
         self.k = 0
-        self.last = [None, None]
+        self.last = [None] * 4
 
     def __call__(self) -> torch.Tensor:
         k = self.k
@@ -277,7 +277,7 @@ class GraphedReduce:
         ev = torch.cuda.Event()
         ev.record()
         self.last[k] = ev
-        self.k ^= 1
+        self.k = (k + 1) % 4
         return self.out
 
     def _check(self, k: int) -> None:
@@ -288,7 +288,7 @@ class GraphedReduce:
             raise ValueError("gradient vector contains NaN or Inf")
 
     def check(self) -> None:
-        for k in range(2):
+        for k in range(4):
             if self.last[k] is not None:
                 self.last[k].synchronize()
                 self._check(k)

@@ -181,8 +181,8 @@ def test_reducer_single_gpu_equals_compress_decode(s2):
 
     d = 1_000_000
     red = s2.S2Reducer(d, rows=3, cols=16384, seed=0)
-    # consecutive reduces alternate the plan's ping-pong tables (decode i zeroes table i+1)
-    for k, alpha in enumerate((0.01, 0.05, 0.001, 0.02, 0.0)):
+    # consecutive reduces rotate the plan's tables over 4 slots (decode i zeroes slot i+2)
+    for k, alpha in enumerate((0.01, 0.05, 0.001, 0.02, 0.0, 0.03, 0.01, 0.2, 0.005)):
         g = o.synthetic_gradient(d, alpha, k, kind="int")
         out = host(red.reduce(cuda(g)))
         ref = o.decompress(o.compress(g, g != 0, 3, 16384, 0))
@@ -490,3 +490,30 @@ def test_block_topk_near_ties(s2):
         band = np.abs(norms - kth) <= 8 * np.spacing(kth)
         assert int(got.sum()) == k
         assert np.array_equal(got[~band], ref[~band]), trial
+
+
+def test_back_to_back_reduces_overlap(s2):
+    """Reduces launched back to back with no host sync (the compress of reduce i+1 overlaps the
+    decode of reduce i through the period-4 buffer rotation), then every output checked; and a
+    reduce whose input IS the previous output (the compress must then wait for that decode)."""
+    import torch
+
+    d = 1_000_003
+    red = s2.S2Reducer(d, rows=3, cols=16384, seed=0)
+    gs = [o.synthetic_gradient(d, a, 40 + k, kind="int") for k, a in enumerate([0.01, 0.03, 0.002, 0.05] * 3)]
+    gt = [cuda(g) for g in gs]
+    outs = [torch.empty(d, device="cuda") for _ in gs]
+    for g, out in zip(gt, outs):
+        red.reduce(g, out=out)
+    torch.cuda.synchronize()
+    for k, (g, out) in enumerate(zip(gs, outs)):
+        ref = o.decompress(o.compress(g, g != 0, 3, 16384, 0))
+        assert np.array_equal(host(out), ref.astype(np.float32)), k
+    # chained: out1 = reduce(g); out2 = reduce(out1) with no sync in between
+    g = gs[0]
+    o1 = red.reduce(gt[0])
+    o2 = red.reduce(o1)
+    r1 = o.decompress(o.compress(g, g != 0, 3, 16384, 0)).astype(np.float32)
+    r2 = o.decompress(o.compress(r1, r1 != 0, 3, 16384, 0)).astype(np.float32)
+    assert np.array_equal(host(o1), r1) and np.array_equal(host(o2), r2)
+    red.check()

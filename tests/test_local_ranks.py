@@ -92,8 +92,8 @@ def test_local_exchange_parity(W, oneshot_maxw, bdiv, rows, cols, push):
                 os.environ[k] = v
     words = torch.zeros(W, dtype=torch.int32, device="cuda")
     grp.set_status(words)
-    # three inputs with different non-zero positions, each reduced twice (both ping-pong buffers):
-    # a stale bitmap or table from the previous call would show up as a parity failure
+    # three inputs with different non-zero positions, each reduced twice (six reduces cover every
+    # table slot of the period-4 rotation): a stale bitmap or table would fail parity
     for kind, base in (("int", 1234), ("normal", 1234), ("normal", 4321)):
         grads = [o.synthetic_gradient(dim, 0.01, r, kind=kind, base_seed=base) for r in range(W)]
         ref, _, mmax = _reference(grads, nb, rows, cols, 0, kind)
@@ -159,3 +159,34 @@ def test_reducer_async_status_raises_on_next_call():
         red.reduce(g)
     red.reduce(g)
     red.check()  # healthy again
+
+
+@pytest.mark.parametrize("W,push", [(2, 0), (4, 1), (8, 1)])
+def test_local_back_to_back(W, push):
+    """Eight W-rank reduces launched back to back with no host sync (every buffer slot of the
+    rotation in flight, compress i+1 overlapping decode i), all outputs checked afterwards."""
+    import torch
+
+    from paper_2110_02140_b200.local import LocalGroup
+
+    dim, rows, cols = 500_009, 3, 4099
+    old = os.environ.get("S2_P2P_PUSH")
+    os.environ["S2_P2P_PUSH"] = str(push)
+    try:
+        grp = LocalGroup(W, dim, rows, cols)
+    finally:
+        if old is None:
+            os.environ.pop("S2_P2P_PUSH")
+        else:
+            os.environ["S2_P2P_PUSH"] = old
+    steps = []
+    for k in range(8):
+        grads = [o.synthetic_gradient(dim, 0.01 * (1 + k % 3), r, kind="int", base_seed=100 * k) for r in range(W)]
+        outs = grp.reduce([torch.from_numpy(g).cuda() for g in grads])
+        steps.append((grads, outs))
+    torch.cuda.synchronize()
+    for k, (grads, outs) in enumerate(steps):
+        ref = o.decompress(o.merge([o.compress(g, g != 0, rows, cols, 0) for g in grads])).astype(np.float32)
+        for r, out in enumerate(outs):
+            assert np.array_equal(out.cpu().numpy(), ref), (k, r)
+    assert grp.errors() == [0] * W
