@@ -168,9 +168,14 @@ int s2_aggregate(s2_plan* plan, float* table, const uint32_t* bitmap, uint32_t* 
  * shares no buffer with the decode of call i and overlaps it through programmatic dependent
  * launch, unless g aliases the previous call's out (then it waits; S2_OVERLAP=0 disables). */
 int s2_reduce(s2_plan* plan, const float* g, float* out, uint64_t* counters, void* stream);
-/* every later s2_reduce's decode writes its S2_STATUS_* bits (0 = healthy) into *status
- * (device memory or mapped pinned host memory; NULL disables) — lets a caller check the
- * previous step without synchronising */
+/* n reduces (gs[k] -> outs[k]), same result as n s2_reduce calls.  With world > 1 they are
+ * pipelined: the compress of step k+1 runs while step k's exchange (NVLink, few SMs) is in
+ * flight, and step k's decode follows it.  Falls back to n plain calls when an input aliases an
+ * earlier output of the batch. */
+int s2_reduce_many(s2_plan* plan, const float* const* gs, float* const* outs, int n, void* stream);
+/* every later s2_reduce's decode ORs its S2_STATUS_* bits (nothing when healthy) into *status
+ * (device memory or mapped pinned host memory; NULL disables; the caller zeroes it) — lets a
+ * caller check earlier steps without synchronising */
 int s2_plan_set_status(s2_plan* plan, uint32_t* status);
 /* device pointer to the counters of the most recent s2_reduce(counters = NULL) */
 const uint64_t* s2_last_counters(const s2_plan* plan);

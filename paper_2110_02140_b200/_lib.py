@@ -68,6 +68,7 @@ SIGNATURES = {
     "s2_comm_check": (c_int, [c_void_p, c_void_p]),
     "s2_aggregate": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "s2_reduce": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "s2_reduce_many": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_void_p]),
     "s2_plan_world": (c_int, [c_void_p]),
     "s2_last_counters": (c_void_p, [c_void_p]),
     "s2_read_counters": (c_int, [c_void_p, c_void_p, c_void_p]),

@@ -604,57 +604,140 @@ int s2_aggregate(s2_plan* plan, float* table, const uint32_t* bitmap, uint32_t* 
   return S2_OK;
 }
 
-int s2_reduce(s2_plan* plan, const float* g, float* out, uint64_t* counters, void* stream) {
+// One reduce = compress -> exchange -> decode.  The three stages are split so that
+// s2_reduce_many can interleave consecutive reduces (compress of step i+1 between the exchange
+// and the decode of step i).
+struct StepBufs {
+  int cur, tc, tz;  // bitmap / union / tsum / inbox slot, table slot, slot the decode zeroes
+  float* table;
+  uint32_t* bitmap;
+  unsigned long long* cnt;
+  const uint32_t* un;
+  const float* dec_table;
+  s2::DecodeHealth health;
+};
+
+static int check_reduce_args(s2_plan* plan, const float* g, const float* out) {
   if (!plan || !g || !out) return fail(S2_EINVAL, "NULL argument to s2_reduce");
   if (reinterpret_cast<uintptr_t>(g) & 15) return fail(S2_EINVAL, "gradient must be 16-byte aligned");
   if (reinterpret_cast<uintptr_t>(out) & 15) return fail(S2_EINVAL, "output must be 16-byte aligned");
   if (plan->world > 1 && !plan->p2p && !plan->comm)
     return fail(S2_EINVAL, "world > 1 needs s2_comm_init (and s2_comm_attach in EXTERNAL mode)");
-  int rc = ensure_scratch(plan);
-  if (rc) return rc;
-  cudaStream_t st = as_stream(stream);
-  const int cur = (int)(plan->step & 1), tc = (int)(plan->step & 3), tz = (int)((plan->step + 2) & 3);
-  float* table = plan->tables[tc];
-  uint32_t* bitmap = plan->p2p ? reinterpret_cast<uint32_t*>(plan->arena + plan->pa.off_bitmap[cur]) : plan->bitmaps[cur];
-  // caller counters: zeroed by memset; plan counters: zeroed by the decode two reduces back
-  unsigned long long* cnt = counters ? reinterpret_cast<unsigned long long*>(counters) : plan->counters[tc];
-  // The compress may overlap the previous reduce's decode (it shares no buffer with it) unless its
-  // input is that decode's output (g aliasing the previous out) — then it waits up front.
   if (plan->overlap < 0) {
     const char* e = getenv("S2_OVERLAP");
     plan->overlap = e ? atoi(e) : 1;
   }
-  const size_t nb = sizeof(float) * (size_t)plan->p.dim;
-  const char* gb = reinterpret_cast<const char*>(g);
-  const char* pb = reinterpret_cast<const char*>(plan->prev_out);
-  const bool alias = pb != nullptr && gb < pb + nb && pb < gb + nb;
-  const bool late = plan->overlap != 0 && !alias;
-  if (plan->ev[0]) cudaEventRecord(plan->ev[0], st);
-  S2_CUDA(s2::launch_compress(plan->p, g, bitmap, table, cnt, S2_MASK_NONZERO, st, counters == nullptr, late),
+  return ensure_scratch(plan);
+}
+
+static bool overlaps(const void* a, const void* b, size_t n) {
+  const char* x = static_cast<const char*>(a);
+  const char* y = static_cast<const char*>(b);
+  return x != nullptr && y != nullptr && x < y + n && y < x + n;
+}
+
+// compress of step plan->step (slots from the step counter); `late`: may overlap its predecessor
+static int stage_compress(s2_plan* plan, const float* g, uint64_t* counters, bool late, cudaStream_t st,
+                          StepBufs* b) {
+  b->cur = (int)(plan->step & 1);
+  b->tc = (int)(plan->step & 3);
+  b->tz = (int)((plan->step + 2) & 3);
+  b->table = plan->tables[b->tc];
+  b->bitmap = plan->p2p ? reinterpret_cast<uint32_t*>(plan->arena + plan->pa.off_bitmap[b->cur]) : plan->bitmaps[b->cur];
+  // caller counters: zeroed by memset; plan counters: zeroed by the decode two reduces back
+  b->cnt = counters ? reinterpret_cast<unsigned long long*>(counters) : plan->counters[b->tc];
+  S2_CUDA(s2::launch_compress(plan->p, g, b->bitmap, b->table, b->cnt, S2_MASK_NONZERO, st, counters == nullptr,
+                              late),
           "s2_reduce/compress");
-  if (plan->ev[1]) cudaEventRecord(plan->ev[1], st);
-  const uint32_t* un = bitmap;
-  s2::DecodeHealth health{nullptr, cnt, plan->status};
-  if (plan->world > 1) {
-    if (plan->p2p) {
-      plan->pa.cur = cur;
-      plan->pa.tcur = tc;
-      S2_CUDA(s2::launch_p2p_aggregate(plan->pa, plan->p2p_grid, st), "s2_reduce/p2p aggregate");
-      un = reinterpret_cast<const uint32_t*>(plan->arena + plan->pa.off_union[cur]);
-      if (plan->pa.oneshot) table = reinterpret_cast<float*>(plan->arena + plan->pa.off_tsum[cur]);  // else in place
-      health.poison = reinterpret_cast<const uint32_t*>(plan->arena + plan->pa.off_error);
-    } else {
-      rc = s2_aggregate(plan, table, bitmap, plan->unionmap, stream);
-      if (rc) return rc;
-      un = plan->unionmap;
-    }
+  return S2_OK;
+}
+
+static int stage_exchange(s2_plan* plan, cudaStream_t st, void* stream, StepBufs* b) {
+  b->un = b->bitmap;
+  b->dec_table = b->table;
+  b->health = s2::DecodeHealth{nullptr, b->cnt, plan->status};
+  if (plan->world == 1) return S2_OK;
+  if (plan->p2p) {
+    plan->pa.cur = b->cur;
+    plan->pa.tcur = b->tc;
+    S2_CUDA(s2::launch_p2p_aggregate(plan->pa, plan->p2p_grid, st), "s2_reduce/p2p aggregate");
+    b->un = reinterpret_cast<const uint32_t*>(plan->arena + plan->pa.off_union[b->cur]);
+    if (plan->pa.oneshot) b->dec_table = reinterpret_cast<const float*>(plan->arena + plan->pa.off_tsum[b->cur]);
+    b->health.poison = reinterpret_cast<const uint32_t*>(plan->arena + plan->pa.off_error);
+    return S2_OK;
   }
-  if (plan->ev[2]) cudaEventRecord(plan->ev[2], st);
-  S2_CUDA(s2::launch_decode(plan->p, un, table, plan->world, out, st, plan->tables[tz], plan->counters[tz], &health),
+  int rc = s2_aggregate(plan, b->table, b->bitmap, plan->unionmap, stream);
+  if (rc) return rc;
+  b->un = plan->unionmap;
+  return S2_OK;
+}
+
+static int stage_decode(s2_plan* plan, float* out, cudaStream_t st, const StepBufs& b) {
+  S2_CUDA(s2::launch_decode(plan->p, b.un, b.dec_table, plan->world, out, st, plan->tables[b.tz],
+                            plan->counters[b.tz], &b.health),
           "s2_reduce/decode");
+  return S2_OK;
+}
+
+int s2_reduce(s2_plan* plan, const float* g, float* out, uint64_t* counters, void* stream) {
+  int rc = check_reduce_args(plan, g, out);
+  if (rc) return rc;
+  cudaStream_t st = as_stream(stream);
+  // The compress may overlap the previous reduce's decode (it shares no buffer with it) unless its
+  // input is that decode's output (g aliasing the previous out) — then it waits up front.
+  const bool late = plan->overlap != 0 && !overlaps(g, plan->prev_out, sizeof(float) * (size_t)plan->p.dim);
+  StepBufs b{};
+  if (plan->ev[0]) cudaEventRecord(plan->ev[0], st);
+  if ((rc = stage_compress(plan, g, counters, late, st, &b))) return rc;
+  if (plan->ev[1]) cudaEventRecord(plan->ev[1], st);
+  if ((rc = stage_exchange(plan, st, stream, &b))) return rc;
+  if (plan->ev[2]) cudaEventRecord(plan->ev[2], st);
+  if ((rc = stage_decode(plan, out, st, b))) return rc;
   if (plan->ev[3]) cudaEventRecord(plan->ev[3], st);
   plan->prev_out = out;
   plan->step += 1;
+  return S2_OK;
+}
+
+int s2_reduce_many(s2_plan* plan, const float* const* gs, float* const* outs, int n, void* stream) {
+  if (!plan || n < 0 || (n > 0 && (!gs || !outs))) return fail(S2_EINVAL, "NULL argument to s2_reduce_many");
+  if (n == 0) return S2_OK;
+  for (int k = 0; k < n; ++k) {
+    int rc = check_reduce_args(plan, gs[k], outs[k]);
+    if (rc) return rc;
+  }
+  // Pipelining needs every input to be independent of every earlier output of the batch, an
+  // exchange to hide (world > 1), the overlap switch on, and no timing events.
+  const size_t nb = sizeof(float) * (size_t)plan->p.dim;
+  bool pipe = plan->world > 1 && plan->overlap != 0 && plan->ev[0] == nullptr;
+  for (int k = 1; pipe && k < n; ++k)
+    for (int j = 0; j < k && pipe; ++j) pipe = !overlaps(gs[k], outs[j], nb);
+  if (!pipe) {
+    for (int k = 0; k < n; ++k) {
+      int rc = s2_reduce(plan, gs[k], outs[k], nullptr, stream);
+      if (rc) return rc;
+    }
+    return S2_OK;
+  }
+  // compress(0) exchange(0) | compress(1) decode(0) exchange(1) | compress(2) decode(1) ... decode(n-1):
+  // each compress runs beside the previous exchange (NVLink- and latency-bound, few SMs); the decode
+  // of step k waits for compress(k+1), which waited for exchange(k) before completing.
+  cudaStream_t st = as_stream(stream);
+  StepBufs prev{}, cur{};
+  int rc;
+  const bool late0 = !overlaps(gs[0], plan->prev_out, nb);
+  if ((rc = stage_compress(plan, gs[0], nullptr, late0, st, &prev))) return rc;
+  if ((rc = stage_exchange(plan, st, stream, &prev))) return rc;
+  plan->step += 1;
+  for (int k = 1; k < n; ++k) {
+    if ((rc = stage_compress(plan, gs[k], nullptr, true, st, &cur))) return rc;
+    if ((rc = stage_decode(plan, outs[k - 1], st, prev))) return rc;
+    if ((rc = stage_exchange(plan, st, stream, &cur))) return rc;
+    plan->step += 1;
+    prev = cur;
+  }
+  if ((rc = stage_decode(plan, outs[n - 1], st, prev))) return rc;
+  plan->prev_out = outs[n - 1];
   return S2_OK;
 }
 

@@ -11,7 +11,7 @@ namespace s2 {
 // zt/zc: the NEXT reduce's sketch table and counters, zeroed here so that the next
 // compress needs no memset (plan ping-pong, s2_reduce); may be null.
 // health (s2_reduce only): a set poison word (exchange timed out) replaces the whole output
-// with NaN; block 0 reports the step's status word.
+// with NaN; block 0 ORs the step's status bits into the status word.
 template <int R, bool BLOCKS>
 __global__ void __launch_bounds__(kThreads)
 k_decode(const uint32_t* __restrict__ bitmap, int64_t dim, int64_t bs,
@@ -26,7 +26,10 @@ k_decode(const uint32_t* __restrict__ bitmap, int64_t dim, int64_t bs,
   if (health.status != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
     uint32_t st = poisoned ? S2_STATUS_EXCHANGE : 0u;
     if (health.counters != nullptr && health.counters[S2_CNT_NONFINITE] != 0ull) st |= S2_STATUS_NONFINITE;
-    *reinterpret_cast<volatile uint32_t*>(health.status) = st;
+    // OR into the word (decodes of one stream are ordered): a batch of reduces sharing one word
+    // keeps any step's error; the caller zeroes the word before arming it
+    volatile uint32_t* w = reinterpret_cast<volatile uint32_t*>(health.status);
+    if (st) *w = *w | st;
   }
   if (poisoned) {  // a peer never arrived: the sums are incomplete, mark every coordinate invalid
     const float nan = __int_as_float(0x7FC00000);

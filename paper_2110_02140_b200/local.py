@@ -68,6 +68,25 @@ class LocalGroup:
             o.record_stream(s)
         return outs
 
+    def reduce_many(self, steps):
+        """steps[k][r] = rank r's gradient of step k; every rank runs s2_reduce_many (the pipelined
+        batch) on its own stream.  Returns outs[k][r]."""
+        n = len(steps)
+        outs = [[torch.empty(self.dim, dtype=torch.float32, device=g.device) for g in st] for st in steps]
+        cur = torch.cuda.current_stream()
+        for r, (p, s) in enumerate(zip(self.plans, self.streams)):
+            s.wait_stream(cur)
+            gp = (ctypes.c_void_p * n)(*[steps[k][r].data_ptr() for k in range(n)])
+            op = (ctypes.c_void_p * n)(*[outs[k][r].data_ptr() for k in range(n)])
+            check(lib.s2_reduce_many(p.handle, gp, op, n, ctypes.c_void_p(s.cuda_stream)), f"reduce_many rank {r}")
+        for s in self.streams:
+            cur.wait_stream(s)
+        for k in range(n):
+            for r, s in enumerate(self.streams):
+                steps[k][r].record_stream(s)
+                outs[k][r].record_stream(s)
+        return outs
+
     def set_status(self, words: torch.Tensor) -> None:
         """words: int32[world] (device or pinned host); rank r's later reduces write their
         S2_STATUS_* bits into words[r]."""

@@ -60,7 +60,7 @@ class _StatusRing:
             self.poll()
         k = self.n % _STATUS_RING
         self.n += 1
-        self.words[k] = -1  # not yet written
+        self.words[k] = 0  # the decodes OR their error bits in
         check(lib.s2_plan_set_status(self.h, ctypes.c_void_p(self.words.data_ptr() + 4 * k)), "set status")
         return k
 
@@ -75,8 +75,6 @@ class _StatusRing:
             if wait:
                 ev.synchronize()
             st = int(self.words[k]) & 0xFFFFFFFF
-            if st == 0xFFFFFFFF:
-                continue  # slot never written (e.g. a graph replayed with another status slot)
             if st & S2_STATUS_EXCHANGE:
                 self.pending.clear()
                 raise RuntimeError("S2 exchange: a cross-rank barrier timed out (a rank died, stalled past the "
@@ -149,6 +147,26 @@ class S2Reducer:
         check(lib.s2_reduce(self.plan.handle, ptr(g), ptr(out), None, stream_ptr(st)), "reduce")
         self._status.launched(k, st)
         return out
+
+    def reduce_many(self, gs, outs=None, stream=None):
+        """``[reduce(g) for g in gs]`` as one pipelined batch (``s2_reduce_many``): with W > 1 the
+        compress of step k+1 runs while step k's NVLink exchange is in flight.  Same outputs."""
+        gs = list(gs)
+        for g in gs:
+            if g.numel() != self.dim:
+                raise ValueError(f"dimension mismatch: mask dim {self.dim}, vector {g.numel()}")
+        self._status.poll()
+        gs = [g if (g.is_cuda and g.dtype == torch.float32 and g.is_contiguous() and g.data_ptr() % 16 == 0)
+              else as_gradient(g, self.device) for g in gs]
+        if outs is None:
+            outs = [torch.empty(self.dim, dtype=torch.float32, device=self.device) for _ in gs]
+        st = stream if stream is not None else torch.cuda.current_stream()
+        gp = (ctypes.c_void_p * len(gs))(*[g.data_ptr() for g in gs])
+        op = (ctypes.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
+        k = self._status.arm()
+        check(lib.s2_reduce_many(self.plan.handle, gp, op, len(gs), stream_ptr(st)), "reduce_many")
+        self._status.launched(k, st)
+        return outs
 
     def check(self) -> None:
         """Wait for every outstanding reduce and raise for NaN/Inf or an exchange timeout."""
@@ -282,6 +300,7 @@ class GraphedReduce:
 
     def _check(self, k: int) -> None:
         st = int(self.words[k]) & 0xFFFFFFFF
+        self.words[k] = 0  # the replay that wrote it has completed; re-arm for the next one
         if st & S2_STATUS_EXCHANGE:
             raise RuntimeError("S2 exchange: a cross-rank barrier timed out; the averaged gradient was set to NaN")
         if st & S2_STATUS_NONFINITE:

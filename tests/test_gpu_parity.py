@@ -517,3 +517,23 @@ def test_back_to_back_reduces_overlap(s2):
     r2 = o.decompress(o.compress(r1, r1 != 0, 3, 16384, 0)).astype(np.float32)
     assert np.array_equal(host(o1), r1) and np.array_equal(host(o2), r2)
     red.check()
+
+
+def test_reduce_many_single_gpu(s2):
+    """reduce_many at W = 1 equals sequential reduces, including a batch whose input aliases an
+    earlier output of the batch (sequential fallback)."""
+    import torch
+
+    d = 300_007
+    red = s2.S2Reducer(d, rows=3, cols=4099, seed=1)
+    gs = [o.synthetic_gradient(d, 0.02, k, kind="int") for k in range(5)]
+    outs = red.reduce_many([cuda(g) for g in gs])
+    for g, out in zip(gs, outs):
+        assert np.array_equal(host(out), o.decompress(o.compress(g, g != 0, 3, 4099, 1)).astype(np.float32))
+    a = torch.empty(d, device="cuda")
+    b = torch.empty(d, device="cuda")
+    red.reduce_many([cuda(gs[0]), a], outs=[a, b])  # step 1 reads step 0's output
+    r0 = o.decompress(o.compress(gs[0], gs[0] != 0, 3, 4099, 1)).astype(np.float32)
+    r1 = o.decompress(o.compress(r0, r0 != 0, 3, 4099, 1)).astype(np.float32)
+    assert np.array_equal(host(a), r0) and np.array_equal(host(b), r1)
+    red.check()

@@ -190,3 +190,36 @@ def test_local_back_to_back(W, push):
         for r, out in enumerate(outs):
             assert np.array_equal(out.cpu().numpy(), ref), (k, r)
     assert grp.errors() == [0] * W
+
+
+@pytest.mark.parametrize("W,push,oneshot_maxw", [(2, 0, 2), (2, 1, 1), (4, 1, 2), (4, 0, 2), (8, 1, 2)])
+def test_local_reduce_many_pipelined(W, push, oneshot_maxw):
+    """s2_reduce_many with W > 1 pipelines the batch (compress k+1 beside exchange k, then decode k);
+    six steps of different inputs, every rank's output of every step against the oracle."""
+    import torch
+
+    from paper_2110_02140_b200.local import LocalGroup
+
+    dim, rows, cols = 400_009, 3, 4099
+    env = {"S2_P2P_PUSH": str(push), "S2_P2P_ONESHOT_MAXW": str(oneshot_maxw)}
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        grp = LocalGroup(W, dim, rows, cols)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k)
+            else:
+                os.environ[k] = v
+    words = torch.zeros(W, dtype=torch.int32, device="cuda")
+    grp.set_status(words)
+    host = [[o.synthetic_gradient(dim, 0.005 * (1 + k % 4), r, kind="int", base_seed=77 * k) for r in range(W)]
+            for k in range(6)]
+    outs = grp.reduce_many([[torch.from_numpy(g).cuda() for g in step] for step in host])
+    torch.cuda.synchronize()
+    for k, step in enumerate(host):
+        ref = o.decompress(o.merge([o.compress(g, g != 0, rows, cols, 0) for g in step])).astype(np.float32)
+        for r in range(W):
+            assert np.array_equal(outs[k][r].cpu().numpy(), ref), (k, r)
+    assert words.cpu().tolist() == [0] * W and grp.errors() == [0] * W

@@ -25,6 +25,7 @@ VARIANTS = {
     "push_oneshot": {"S2_P2P_PUSH": "1"},      # push one-shot
     "nccl": {"S2_AGG": "nccl"},                # NCCL all-reduce + all-gather + OR kernel (north-star literal)
     "graph": {"S2_CHECK_GRAPH": "1"},          # CUDA-graph replay of the whole reduce
+    "many": {"S2_CHECK_MANY": "1"},            # pipelined batch (reduce_many)
     "blocks": {"S2_CHECK_NUM_BLOCKS": "62500"},  # block bitmap (b < d, 32 elements per block)
 }
 

@@ -50,6 +50,7 @@ report = {"world": world, "dim": a.dim, "graph": graphed is not None}
 # output checked: a stale bitmap or table from the previous call of the same ping-pong
 # parity would show up as a parity failure
 CASES = (("int", "int", 1234), ("normal", "normal", 1234), ("normal_b", "normal", 4321))
+MANY = os.environ.get("S2_CHECK_MANY") == "1"  # the pipelined batch API (reduce_many) instead
 for name, kind, base in CASES:
     grads = [o.synthetic_gradient(a.dim, a.alpha, r, kind=kind, base_seed=base) for r in range(world)]
     ps = [o.compress(g, o.nonzero_flags(g, nb), a.rows, a.cols, 0) for g in grads]
@@ -69,8 +70,13 @@ for name, kind, base in CASES:
     outside = np.ones(a.dim, bool)
     outside[union] = False
     oks_rep, errs, hashes = [], [], []
-    for rep in range(2):  # twice: both ping-pong buffers
-        if graphed is None:
+    if MANY:  # four copies of the input in one pipelined batch, every output checked
+        batch = red.reduce_many([torch.from_numpy(grads[rank]).cuda() for _ in range(4)])
+        many_outs = [x.cpu().numpy() for x in batch]
+    for rep in range(4 if MANY else 2):  # every buffer slot of the rotation
+        if MANY:
+            out = many_outs[rep]
+        elif graphed is None:
             out = red.reduce(torch.from_numpy(grads[rank]).cuda()).cpu().numpy()
         else:
             g_static.copy_(torch.from_numpy(grads[rank]))
@@ -86,7 +92,7 @@ for name, kind, base in CASES:
     hs = [None] * world
     dist.all_gather_object(hs, hashes)
     report[name] = {"parity": all(oks_rep), "max_err": max(errs),
-                    "replicated": all(len({h[k] for h in hs}) == 1 for k in range(2)),
+                    "replicated": all(len({h[k] for h in hs}) == 1 for k in range(len(hashes))),
                     "nnz_union": int(m.flags.sum())}
 oks = [None] * world
 dist.all_gather_object(oks, all(report[c[0]]["parity"] and report[c[0]]["replicated"] for c in CASES))
