@@ -489,7 +489,7 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=120.0, help="max seconds of timed reference steps")
     ap.add_argument("--alpha", type=float, default=None, help="override the config's non-zero fraction")
     ap.add_argument("--cols", type=int, default=None, help="override the config's sketch width")
-    ap.add_argument("--pipeline", type=int, default=4,
+    ap.add_argument("--pipeline", type=int, default=8,
                     help="W > 1: reduces per s2_reduce_many batch (1 = one s2_reduce per step)")
     args = ap.parse_args()
     ws = int(os.environ.get("WORLD_SIZE", "1"))

@@ -10,6 +10,6 @@ for f in sys.argv[1:]:
         print(f, "ERR", e)
         continue
     ph = d.get("phases", {})
-    print(f, f"ms={d.get('ms_per_step')} value={d.get('value')} GB/s",
+    print(f, f"ms={d.get('ms_per_step')} lat={d.get('latency_ms_per_reduce')} value={d.get('value')} GB/s",
           " ".join(f"{k}={v.get('ms')}" for k, v in ph.items()),
           f"e2e={d.get('e2e', {}).get('value')}", f"frac={d.get('roofline', {}).get('frac')}")
