@@ -131,6 +131,34 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples_under_load": in_load, "samples": len(self.rows)}
 
 
+# Measured ceilings of the two non-HBM resources the kernels can saturate (1 B200, this pool):
+# random 4-byte L2 gathers — one L1->crossbar request per SM cycle, shared with every written
+# 32-byte sector (profiles/r02_dsmem_bench.json "l2_gather", profiles/r02_ab_decode_bulk_qr.txt) —
+# and random fp32 red.global.add into an L2-resident table (profiles/r02_atomics_bench.json).
+L2_REQ_PER_S = 295.5e9
+L2_RED_PER_S = 185.0e9
+NVLINK_A2A_GBS = 646.0
+
+
+def kernel_floors(d, rows, cols, words_bytes, nnz, union, hbm_peak):
+    """Lower bounds on the compress / decode durations from the measured ceilings: HBM bytes at the
+    copy peak; compress REDs (rows x nnz) at the L2 RED rate; decode L1->xbar requests (rows x union
+    gathers + written output / next-table / bitmap sectors) at the request rate."""
+    table_bytes = 4 * rows * cols
+    hbm_c = (4 * d + words_bytes + table_bytes) / (hbm_peak * 1e9) * 1e6
+    red_c = rows * nnz / L2_RED_PER_S * 1e6
+    req = rows * union + (4 * d + table_bytes + words_bytes) / 32
+    hbm_d = (4 * d + 2 * table_bytes + words_bytes) / (hbm_peak * 1e9) * 1e6
+    req_d = req / L2_REQ_PER_S * 1e6
+    return {
+        "compress": {"us": round(max(hbm_c, red_c), 2), "bound": "hbm" if hbm_c >= red_c else "l2 red",
+                     "hbm_us": round(hbm_c, 2), "red_us": round(red_c, 2), "reds": rows * nnz},
+        "decode": {"us": round(max(hbm_d, req_d), 2), "bound": "hbm" if hbm_d >= req_d else "l1-xbar requests",
+                   "hbm_us": round(hbm_d, 2), "request_us": round(req_d, 2), "requests": int(req),
+                   "union": union},
+    }
+
+
 # ----------------------------------------------------------------- reference
 
 
@@ -366,6 +394,9 @@ def ours(args, cfg):
         phases["decode"] += ev[2].elapsed_time(ev[3])
     check(lib.s2_plan_set_timing_events(h, None, 0))
     phases = {k: max_over_ranks(v / nph) for k, v in phases.items()}
+    # union coordinates the decode queried (non-zeros of a decoded output; an exactly-zero
+    # median of real-valued estimates does not occur at these sizes)
+    union = int(max_over_ranks(float((outs[0] != 0).sum().item())))
     del outs
 
     # e2e: pinned host gradient in, pinned host result out, every step's H2D and D2H inside the
@@ -438,15 +469,22 @@ def ours(args, cfg):
             ncu = {"us": nd, "achieved": round(na, 1), "frac": round(na / hbm_peak, 4),
                    "source": tj.get("_source", "profiles/traffic.json")}
     phase_out = {}
+    nnz = int(round(cfg["alpha"] * (cfg["grid"][0] if cfg.get("grid") else d))) * (cfg["grid"][1] if cfg.get("grid") else 1)
+    floors = kernel_floors(d, rows, cols, words_bytes, nnz, union, hbm_peak)
     for k in ("compress", "decode"):
         a = alg[k] / (phases[k] * 1e-3) / 1e9
+        fl = floors[k]
         phase_out[k] = {"ms": round(phases[k], 5), "GB/s": round(a, 1), "frac": round(a / hbm_peak, 4),
-                        "algorithmic_bytes": alg[k]}
+                        "algorithmic_bytes": alg[k],
+                        "floor": dict(fl, frac=round(fl["us"] / (phases[k] * 1e3), 4))}
     if world > 1:
         bus = 2 * (world - 1) / world * table_bytes + (world - 1) / world * world * words_bytes
-        phase_out["aggregate"] = {"ms": round(phases["aggregate"], 5),
-                                  "bus_GB/s": round(bus / (phases["aggregate"] * 1e-3) / 1e9, 1),
-                                  "bus_bytes": bus}
+        bus_gbs = bus / (phases["aggregate"] * 1e-3) / 1e9
+        phase_out["aggregate"] = {"ms": round(phases["aggregate"], 5), "bus_GB/s": round(bus_gbs, 1),
+                                  "bus_bytes": bus, "frac_of_900": round(bus_gbs / 900.0, 4),
+                                  "frac_of_measured": round(bus_gbs / NVLINK_A2A_GBS, 4),
+                                  "measured_peak": f"{NVLINK_A2A_GBS} GB/s: all-to-all SM stores, 32 MiB per peer, "
+                                                   "W=4 (profiles/r02_nvlink_bench_w4.json)"}
     value = B / (ms * 1e-3) / 1e9  # per GPU (BASELINE.json metric); job_GBps = world * value
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
@@ -457,7 +495,7 @@ def ours(args, cfg):
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(ach / hbm_peak, 4), "traffic": traffic, "peak_kind": peak_kind,
                      "bytes_per_launch": alg[dom], "timing": "CUDA events around the kernel inside the step",
-                     "ncu": ncu},
+                     "ncu": ncu, "measured_floor": phase_out[dom]["floor"]},
         "phases": phase_out,
         "e2e": {"value": round(B / (ms_e2e * 1e-3) / 1e9, 3), "unit": "GB/s", "ms_per_step": round(ms_e2e, 4),
                 "h2d_bytes_per_step": B, "d2h_bytes_per_step": B,

@@ -223,3 +223,46 @@ def test_local_reduce_many_pipelined(W, push, oneshot_maxw):
         for r in range(W):
             assert np.array_equal(outs[k][r].cpu().numpy(), ref), (k, r)
     assert words.cpu().tolist() == [0] * W and grp.errors() == [0] * W
+
+
+@pytest.mark.parametrize("W,push", [(2, 0), (4, 1)])
+def test_local_exchange_beside_concurrent_compute(W, push):
+    """The exchange kernels spin on cross-rank flags while other streams keep the SMs busy (the
+    DDP situation: the comm hook's stream overlaps backward kernels).  A side stream runs large
+    matmuls launched before and between the reduces; every reduce must still complete — no
+    barrier timeout — and match the oracle bit for bit."""
+    import torch
+
+    from paper_2110_02140_b200.local import LocalGroup
+
+    dim, rows, cols = 1_000_003, 3, 20011
+    old = os.environ.get("S2_P2P_PUSH")
+    os.environ["S2_P2P_PUSH"] = str(push)
+    try:
+        grp = LocalGroup(W, dim, rows, cols, timeout_s=20.0)
+    finally:
+        if old is None:
+            os.environ.pop("S2_P2P_PUSH")
+        else:
+            os.environ["S2_P2P_PUSH"] = old
+    words = torch.zeros(W, dtype=torch.int32, device="cuda")
+    grp.set_status(words)
+    side = torch.cuda.Stream()
+    a = torch.randn(4096, 4096, device="cuda")
+    b = torch.randn(4096, 4096, device="cuda")
+    cs = []
+    steps = []
+    for k in range(4):
+        with torch.cuda.stream(side):
+            for _ in range(4):
+                cs.append(a @ b)  # occupies every SM for tens of microseconds per launch
+        grads = [o.synthetic_gradient(dim, 0.01, r, kind="int", base_seed=31 * k + 5) for r in range(W)]
+        outs = grp.reduce([torch.from_numpy(g).cuda() for g in grads])
+        steps.append((grads, outs))
+    torch.cuda.synchronize()
+    for k, (grads, outs) in enumerate(steps):
+        ref = o.decompress(o.merge([o.compress(g, g != 0, rows, cols, 0) for g in grads])).astype(np.float32)
+        for r, out in enumerate(outs):
+            assert np.array_equal(out.cpu().numpy(), ref), (k, r)
+    assert words.cpu().tolist() == [0] * W and grp.errors() == [0] * W
+    assert torch.isfinite(cs[-1]).all()
