@@ -163,8 +163,8 @@ int s2_aggregate(s2_plan* plan, float* table, const uint32_t* bitmap, uint32_t* 
 /* the whole reduce: compress -> aggregate -> decode (÷ world) using plan-owned
  * scratch; out = float32[dim] averaged gradient.  counters may be NULL (then the
  * plan's own are used, see s2_last_counters).  Plan-owned buffers rotate with period 4
- * (call i uses table / counters slot i % 4 and bitmap slot i % 2; its decode zeroes slot
- * (i+2) % 4), so a CUDA graph must capture a multiple of 4 calls.  The compress of call i+1
+ * (call i uses table / counters slot i % 4 and bitmap slot i % 2 (i % 4 with an exchange
+ * arena); its decode zeroes slot (i+2) % 4), so a CUDA graph must capture a multiple of 4 calls.  The compress of call i+1
  * shares no buffer with the decode of call i and overlaps it through programmatic dependent
  * launch, unless g aliases the previous call's out (then it waits; S2_OVERLAP=0 disables). */
 int s2_reduce(s2_plan* plan, const float* g, float* out, uint64_t* counters, void* stream);

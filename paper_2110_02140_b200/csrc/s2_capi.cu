@@ -23,9 +23,10 @@ struct s2_plan {
   int rank = 0;
   ncclComm_t comm = nullptr;
   // plan-owned scratch for s2_reduce / s2_aggregate.  Reduce i uses sketch table and counters
-  // slot i % 4 and bitmap slot i % 2; its decode zeroes table / counters slot (i + 2) % 4, so the
-  // hot path has no memset launches and the compress of reduce i+1 (slots (i+1) % 4, (i+1) % 2)
-  // shares no buffer with the decode of reduce i and may overlap it (late_wait).
+  // slot i % 4 and bitmap slot i % 2 (i % 4 in the exchange arena); its decode zeroes table /
+  // counters slot (i + 2) % 4 in its prologue (fenced before it lets dependents launch), so the
+  // hot path has no memset launches and the compress of reduce i+1 (or i+2 in s2_reduce_many's
+  // two-stream schedule) may overlap the decode of reduce i (late_wait).
   static constexpr int kTableSlots = 4;
   float* tables[kTableSlots] = {};
   unsigned long long* counters[kTableSlots] = {};
@@ -47,6 +48,11 @@ struct s2_plan {
   bool arena_owned = false;  // cudaMalloc'd here (IPC) vs attached by the caller (EXTERNAL)
   int opt_grid = 0;          // s2_comm_set_options
   double opt_timeout_s = 0;
+  // s2_reduce_many's exchange stream (high priority) and its fork/join events
+  cudaStream_t xstream = nullptr;
+  static constexpr int kPipeEvents = 4;
+  cudaEvent_t ev_c[kPipeEvents] = {};  // compress k done (main stream)
+  cudaEvent_t ev_x[kPipeEvents] = {};  // exchange k done (exchange stream)
 };
 
 namespace {
@@ -206,6 +212,15 @@ static void free_p2p(s2_plan* p) {
 }
 
 void s2_plan_destroy(s2_plan* plan) {
+  if (plan && plan->xstream) {
+    cudaStreamSynchronize(plan->xstream);
+    cudaStreamDestroy(plan->xstream);
+    for (int k = 0; k < s2_plan::kPipeEvents; ++k) {
+      cudaEventDestroy(plan->ev_c[k]);
+      cudaEventDestroy(plan->ev_x[k]);
+    }
+    plan->xstream = nullptr;
+  }
   if (!plan) return;
   free_p2p(plan);
   if (plan->comm) ncclCommDestroy(plan->comm);
@@ -330,7 +345,7 @@ static int ensure_scratch(s2_plan* p) {
 static int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 // Arena layout (identical on every rank):
-//   tables[4] | bitmaps[2] | unions[2] | flags_a[W*8G] | flags_b[W*8G] | epochs[8G] | error | tsum[2]?
+//   tables[4] | bitmaps[4] | unions[2] | flags_a[W*8G] | flags_b[W*8G] | epochs[8G] | error | tsum[2]?
 //   | inbox[2]? (push exchange)
 // (flag and epoch slots for exchange grids of up to 8 CTAs per SM)
 static int64_t layout_p2p(s2_plan* plan, int W, int G) {
@@ -344,7 +359,7 @@ static int64_t layout_p2p(s2_plan* plan, int W, int G) {
     return o;
   };
   for (int k = 0; k < s2_plan::kTableSlots; ++k) a.off_table[k] = take(cells * 4);
-  for (int k = 0; k < 2; ++k) a.off_bitmap[k] = take(words * 4);
+  for (int k = 0; k < s2_plan::kTableSlots; ++k) a.off_bitmap[k] = take(words * 4);
   for (int k = 0; k < 2; ++k) a.off_union[k] = take(words * 4);
   a.off_flags_a = take((int64_t)W * 8 * G * 4);
   a.off_flags_b = take((int64_t)W * 8 * G * 4);
@@ -643,7 +658,7 @@ static int stage_compress(s2_plan* plan, const float* g, uint64_t* counters, boo
   b->tc = (int)(plan->step & 3);
   b->tz = (int)((plan->step + 2) & 3);
   b->table = plan->tables[b->tc];
-  b->bitmap = plan->p2p ? reinterpret_cast<uint32_t*>(plan->arena + plan->pa.off_bitmap[b->cur]) : plan->bitmaps[b->cur];
+  b->bitmap = plan->p2p ? reinterpret_cast<uint32_t*>(plan->arena + plan->pa.off_bitmap[b->tc]) : plan->bitmaps[b->cur];
   // caller counters: zeroed by memset; plan counters: zeroed by the decode two reduces back
   b->cnt = counters ? reinterpret_cast<unsigned long long*>(counters) : plan->counters[b->tc];
   S2_CUDA(s2::launch_compress(plan->p, g, b->bitmap, b->table, b->cnt, S2_MASK_NONZERO, st, counters == nullptr,
@@ -719,12 +734,65 @@ int s2_reduce_many(s2_plan* plan, const float* const* gs, float* const* outs, in
     }
     return S2_OK;
   }
-  // compress(0) exchange(0) | compress(1) decode(0) exchange(1) | compress(2) decode(1) ... decode(n-1):
-  // each compress runs beside the previous exchange (NVLink- and latency-bound, few SMs); the decode
-  // of step k waits for compress(k+1), which waited for exchange(k) before completing.
   cudaStream_t st = as_stream(stream);
-  StepBufs prev{}, cur{};
   int rc;
+  static int streams = -1;  // S2_PIPE_STREAMS=1: the one-stream schedule below (A/B switch)
+  if (streams < 0) {
+    const char* e = getenv("S2_PIPE_STREAMS");
+    streams = e ? atoi(e) : 2;
+  }
+  if (plan->p2p && n > 1 && streams == 2) {
+    // Two streams.  Main: compress(0) compress(1) decode(0) compress(2) decode(1) ... decode(n-1);
+    // exchange stream: exchange(0) exchange(1) ..., exchange(k) after compress(k), decode(k) after
+    // exchange(k).  Every exchange (NVLink- and latency-bound, half the SMs, mostly spinning) runs
+    // beside the HBM-bound compress AND decode of the neighbouring reduces, so a batch costs about
+    // (compress + decode) per reduce once the exchange is shorter than that.  Buffer safety: table
+    // and bitmap slots rotate over 4, union / tsum / inbox over 2; exchange(k+1) touches slots k+1
+    // only, while decode(k) reads slots k and zeroes table slot k+2, whose compress follows it
+    // (DESIGN.md §7).
+    if (!plan->xstream) {
+      int lo = 0, hi = 0;
+      S2_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi), "stream priorities");
+      S2_CUDA(cudaStreamCreateWithPriority(&plan->xstream, cudaStreamNonBlocking, hi), "exchange stream");
+      for (int k = 0; k < s2_plan::kPipeEvents; ++k) {
+        S2_CUDA(cudaEventCreateWithFlags(&plan->ev_c[k], cudaEventDisableTiming), "event");
+        S2_CUDA(cudaEventCreateWithFlags(&plan->ev_x[k], cudaEventDisableTiming), "event");
+      }
+    }
+    cudaStream_t xs = plan->xstream;
+    StepBufs prev{}, cur{};
+    auto exchange = [&](StepBufs* b, int k) -> int {
+      cudaEvent_t ec = plan->ev_c[k % s2_plan::kPipeEvents], ex = plan->ev_x[k % s2_plan::kPipeEvents];
+      S2_CUDA(cudaEventRecord(ec, st), "record compress");
+      S2_CUDA(cudaStreamWaitEvent(xs, ec, 0), "exchange waits compress");
+      int r = stage_exchange(plan, xs, xs, b);
+      if (r) return r;
+      S2_CUDA(cudaEventRecord(ex, xs), "record exchange");
+      return S2_OK;
+    };
+    auto decode = [&](const StepBufs& b, float* out, int k) -> int {
+      S2_CUDA(cudaStreamWaitEvent(st, plan->ev_x[k % s2_plan::kPipeEvents], 0), "decode waits exchange");
+      return stage_decode(plan, out, st, b);
+    };
+    const bool late0 = !overlaps(gs[0], plan->prev_out, nb);
+    if ((rc = stage_compress(plan, gs[0], nullptr, late0, st, &prev))) return rc;
+    if ((rc = exchange(&prev, 0))) return rc;
+    plan->step += 1;
+    for (int k = 1; k < n; ++k) {
+      if ((rc = stage_compress(plan, gs[k], nullptr, true, st, &cur))) return rc;
+      if ((rc = exchange(&cur, k))) return rc;
+      if ((rc = decode(prev, outs[k - 1], k - 1))) return rc;
+      plan->step += 1;
+      prev = cur;
+    }
+    if ((rc = decode(prev, outs[n - 1], n - 1))) return rc;
+    plan->prev_out = outs[n - 1];
+    return S2_OK;
+  }
+  // one stream: compress(0) exchange(0) | compress(1) decode(0) exchange(1) | compress(2) decode(1) ...
+  // decode(n-1): each compress runs beside the previous exchange; the decode of step k waits for
+  // compress(k+1), which waited for exchange(k) before completing.
+  StepBufs prev{}, cur{};
   const bool late0 = !overlaps(gs[0], plan->prev_out, nb);
   if ((rc = stage_compress(plan, gs[0], nullptr, late0, st, &prev))) return rc;
   if ((rc = stage_exchange(plan, st, stream, &prev))) return rc;

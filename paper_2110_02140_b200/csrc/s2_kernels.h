@@ -62,14 +62,14 @@ cudaError_t launch_pairs(const Plan& p, const int64_t* idx, const float* vals, i
 // NVLink peer-memory exchange (s2_p2p.cu)
 struct P2PArgs {
   char* base[kMaxWorld];  // arena base of every rank (self included), mapped in this process
-  int64_t off_table[4];   // sketch tables rotate over 4 slots (s2_reduce), the rest over 2
-  int64_t off_bitmap[2], off_union[2];
+  int64_t off_table[4];   // sketch tables and bitmaps rotate over 4 slots (s2_reduce), the rest over 2
+  int64_t off_bitmap[4], off_union[2];
   int64_t off_flags_a, off_flags_b, off_epoch, off_error;
   int64_t off_tsum[2];  // one-shot: private summed tables
   int64_t cells;  // table cells, padded to a multiple of 4 * world
   int64_t words;  // bitmap words, padded to a multiple of 4 * world
-  int world, rank, cur;  // cur: slot of bitmap / union / tsum / inbox (step & 1)
-  int tcur;              // table slot (step & 3)
+  int world, rank, cur;  // cur: slot of union / tsum / inbox (step & 1)
+  int tcur;              // table and bitmap slot (step & 3)
   int oneshot;                    // 1: one-shot exchange (single barrier), 0: two-shot
   int push;                       // 1: data pushed into the peers' inboxes before each flag (else pulled after)
   int64_t off_inbox[2];           // push: W slots (one-shot: whole table+bitmap; two-shot: one slice)

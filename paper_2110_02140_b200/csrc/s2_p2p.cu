@@ -142,7 +142,7 @@ __device__ __forceinline__ void reduce_batch(const P2PArgs& a, int64_t i0, int64
   for (int k = 0; k < B; ++k) {
     const int64_t i = i0 + (int64_t)k * kP2PThreads;
     if (i < hi) {
-      const int64_t off = i < t4 ? a.off_table[tc] + (me * t4 + i) * 16 : a.off_bitmap[cur] + (me * w4 + i - t4) * 16;
+      const int64_t off = i < t4 ? a.off_table[tc] + (me * t4 + i) * 16 : a.off_bitmap[tc] + (me * w4 + i - t4) * 16;
 #pragma unroll
       for (int q = 0; q < W; ++q) v[k][q] = __ldcg(reinterpret_cast<const uint4*>(a.base[q] + off));
     }
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(kP2PThreads) k_p2p_oneshot(const __grid_consta
     for (int k = 0; k < B; ++k) {
       const int64_t i = i0 + (int64_t)k * kP2PThreads;
       if (i < hi) {
-        const int64_t off = i < t4 ? a.off_table[tc] + i * 16 : a.off_bitmap[cur] + (i - t4) * 16;
+        const int64_t off = i < t4 ? a.off_table[tc] + i * 16 : a.off_bitmap[tc] + (i - t4) * 16;
 #pragma unroll
         for (int q = 0; q < W; ++q) v[k][q] = __ldcg(reinterpret_cast<const uint4*>(a.base[q] + off));
       }
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(kP2PThreads) k_p2p_push_oneshot(const __grid_c
   chunk_of(t4 + w4, lo, hi);
   const int64_t in_me = a.off_inbox[cur] + me * slot;
   for (int64_t i = lo + threadIdx.x; i < hi; i += kP2PThreads) {
-    const int64_t off = i < t4 ? a.off_table[tc] + i * 16 : a.off_bitmap[cur] + (i - t4) * 16;
+    const int64_t off = i < t4 ? a.off_table[tc] + i * 16 : a.off_bitmap[tc] + (i - t4) * 16;
     const uint4 v = __ldcg(reinterpret_cast<const uint4*>(a.base[me] + off));
 #pragma unroll
     for (int q = 0; q < W; ++q)
@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(kP2PThreads) k_p2p_push_oneshot(const __grid_c
     for (int k = 0; k < B; ++k) {
       const int64_t i = i0 + (int64_t)k * kP2PThreads;
       if (i < hi) {
-        const int64_t own = i < t4 ? a.off_table[tc] + i * 16 : a.off_bitmap[cur] + (i - t4) * 16;
+        const int64_t own = i < t4 ? a.off_table[tc] + i * 16 : a.off_bitmap[tc] + (i - t4) * 16;
 #pragma unroll
         for (int q = 0; q < W; ++q)
           v[k][q] = __ldcg(reinterpret_cast<const uint4*>(
@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(kP2PThreads) k_p2p_push_twoshot(const __grid_c
   chunk_of(t4 + w4, lo, hi);
   // vector i of slice s in this rank's table / bitmap (local) and union
   auto src = [&](int sl, int64_t i) { return i < t4 ? a.off_table[tc] + (sl * t4 + i) * 16
-                                                    : a.off_bitmap[cur] + (sl * w4 + i - t4) * 16; };
+                                                    : a.off_bitmap[tc] + (sl * w4 + i - t4) * 16; };
   auto dst = [&](int sl, int64_t i) { return i < t4 ? a.off_table[tc] + (sl * t4 + i) * 16
                                                     : a.off_union[cur] + (sl * w4 + i - t4) * 16; };
   // reduce-scatter, push: slice q of my chunk -> inbox slot [me] of rank q

@@ -10,12 +10,17 @@ against the oracle (sparse.py:174-196) and proxy the W = 8 union density for the
 The exchange grids of all W ranks must be co-resident (a CTA waits for the same CTA
 index of the other ranks): each rank's exchange kernel gets ``exchange_grid`` CTAs of
 1024 threads (one SM each), default SMs // (2W), so W x G SMs at most spin while the
-rest of the GPU runs the ranks' compress and decode kernels.
+rest of the GPU runs the ranks' compress and decode kernels.  The ranks' streams (two per
+rank under ``reduce_many``) must not share CUDA hardware work queues, or a spinning exchange
+can queue in front of work another rank waits for: set ``CUDA_DEVICE_MAX_CONNECTIONS`` >= 2W + 2
+before CUDA initialises (tests/conftest.py sets 32).
 """
 
 from __future__ import annotations
 
 import ctypes
+import os
+import warnings
 
 import torch
 
@@ -28,6 +33,10 @@ class LocalGroup:
                  exchange_grid: int = 0, timeout_s: float = 20.0):
         if not 2 <= world <= 8:
             raise ValueError("world must be in [2, 8]")
+        conns = int(os.environ.get("CUDA_DEVICE_MAX_CONNECTIONS", "8"))
+        if conns < 2 * world + 2:
+            warnings.warn(f"CUDA_DEVICE_MAX_CONNECTIONS={conns} < {2 * world + 2}: the {world} ranks' streams share "
+                          "hardware queues and a pipelined exchange may time out (see module docstring)")
         self.world, self.dim = int(world), int(dim)
         dev = torch.device("cuda", torch.cuda.current_device())
         sms = torch.cuda.get_device_properties(dev).multi_processor_count

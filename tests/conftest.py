@@ -1,7 +1,14 @@
 import os
 import sys
 
-import pytest
+# The single-GPU multi-rank harness (tests/test_local_ranks.py) runs W ranks x 2 streams
+# (s2_reduce_many's exchange stream) in one process.  With CUDA's default 8 hardware work queues,
+# streams share queues and a spinning exchange kernel can sit in front of the compress another
+# rank's exchange waits for (false dependency -> barrier timeout).  Must be set before the CUDA
+# context exists.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
+import pytest  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
