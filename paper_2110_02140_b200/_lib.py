@@ -13,7 +13,7 @@ import os
 from ctypes import POINTER, c_char_p, c_float, c_int, c_int8, c_int64, c_uint64, c_void_p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libs2.so")
+LIB_PATH = os.environ.get("S2_LIB") or os.path.join(_HERE, "libs2.so")  # S2_LIB: A/B of two builds
 
 S2_OK = 0
 S2_EINVAL = 1
