@@ -44,8 +44,13 @@ k_decode(const uint32_t* __restrict__ bitmap, int64_t dim, int64_t bs,
   __shared__ __align__(16) float s_v[kWarps][kTile];
   const int wib = threadIdx.x >> 5;
   const int64_t ntiles = (dim + kTile - 1) / kTile;
+  if (BLOCKS) {  // block bitmaps: decode_tile_clear keeps the stage zero outside the set positions
+    float4* v4 = reinterpret_cast<float4*>(s_v[wib]);
+    for (int k = threadIdx.x & 31; k < kTile / 4; k += 32) v4[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncwarp();
+  }
   DecodeCtx c{bitmap, table, out, dim, bs, workers, inv_workers, workers_pow2};
-  decode_range<R, BLOCKS>(c, (int64_t)blockIdx.x * kWarps + wib, (int64_t)gridDim.x * kWarps, ntiles, hp, s_q[wib],
+  decode_range<R, BLOCKS, BLOCKS>(c, (int64_t)blockIdx.x * kWarps + wib, (int64_t)gridDim.x * kWarps, ntiles, hp, s_q[wib],
                           s_v[wib]);
 }
 

@@ -185,19 +185,65 @@ __device__ __forceinline__ void decode_tile(const DecodeCtx& c, int64_t base, ui
   __syncwarp();
 }
 
+// decode_tile with a value stage that is zero everywhere except the current tile's set
+// positions: the dense output leaves as 8 unmasked LDS.128 + STG.128 per lane (no per-chunk
+// nibble shuffles and selects); the previous tile's positions (still in q) are cleared first.
+// The stage must be zero on the first call.  Used for block bitmaps (LSTM row bitmap step
+// -2.3 %); at element bitmaps the extra shared-memory reads cost more than the selects save
+// (ResNet-50 step +1-2 %, profiles/r02_ab_decode_clear.txt).
+template <int R>
+__device__ __forceinline__ void decode_tile_clear(const DecodeCtx& c, int64_t base, uint32_t word,
+                                                  const HashParams& hp, uint16_t* q, float* vals, int& prev_total) {
+  const int lane = threadIdx.x & 31;
+  const int64_t dim = c.dim;
+  const int cnt = __popc(word);
+  int pre = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int n = __shfl_up_sync(kFull, pre, o);
+    if (lane >= o) pre += n;
+  }
+  const int total = __shfl_sync(kFull, pre, 31);
+  pre -= cnt;
+  for (int s = lane; s < prev_total; s += 32) vals[q[s]] = 0.f;
+  __syncwarp();
+  for (uint32_t w = word; w; w &= w - 1u) q[pre++] = (uint16_t)(lane * 32 + (__ffs(w) - 1));
+  __syncwarp();
+  for (int s = lane; s < total; s += 32) {
+    const int pos = q[s];
+    const float qv = query_one<R>((uint64_t)(base + pos), c.table, hp);
+    vals[pos] = c.workers_pow2 ? qv * c.inv_workers : __fdiv_rn(qv, c.workers);
+  }
+  prev_total = total;
+  __syncwarp();
+  if (base + kDecTile <= dim) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      __stcs(reinterpret_cast<float4*>(c.out + base + k * 128 + lane * 4),
+             *reinterpret_cast<const float4*>(vals + k * 128 + lane * 4));
+  } else {
+    for (int64_t e = lane; base + e < dim; e += 32) c.out[base + e] = vals[e];
+  }
+  __syncwarp();
+}
+
 // Decode warp tiles t0, t0+tstep, ... < tend (one warp); the bitmap word is prefetched one
-// tile ahead.
-template <int R, bool BLOCKS>
+// tile ahead.  CLEAR: decode_tile_clear (the caller zeroes the stage first).
+template <int R, bool BLOCKS, bool CLEAR = false>
 __device__ __forceinline__ void decode_range(const DecodeCtx& c, int64_t t0, int64_t tstep, int64_t tend,
                                              const HashParams& hp, uint16_t* q, float* vals) {
   const int lane = threadIdx.x & 31;
   const int64_t nelem_words = (c.dim + 31) / 32;
   int64_t t = t0;
+  int prev_total = 0;
   uint32_t wnext = t < tend ? decode_word<BLOCKS>(c.bitmap, t, lane, c.dim, c.bs, nelem_words) : 0u;
   for (; t < tend; t += tstep) {
     const uint32_t word = wnext;
     if (t + tstep < tend) wnext = decode_word<BLOCKS>(c.bitmap, t + tstep, lane, c.dim, c.bs, nelem_words);
-    decode_tile<R>(c, t * kDecTile, word, hp, q, vals);
+    if constexpr (CLEAR)
+      decode_tile_clear<R>(c, t * kDecTile, word, hp, q, vals, prev_total);
+    else
+      decode_tile<R>(c, t * kDecTile, word, hp, q, vals);
   }
 }
 
