@@ -25,7 +25,9 @@ VARIANTS = {
     "push_oneshot": {"S2_P2P_PUSH": "1"},      # push one-shot
     "nccl": {"S2_AGG": "nccl"},                # NCCL all-reduce + all-gather + OR kernel (north-star literal)
     "graph": {"S2_CHECK_GRAPH": "1"},          # CUDA-graph replay of the whole reduce
-    "many": {"S2_CHECK_MANY": "1"},            # pipelined batch (reduce_many)
+    "many": {"S2_CHECK_MANY": "1"},            # pipelined batch (reduce_many, two streams)
+    "many_pull": {"S2_CHECK_MANY": "1", "S2_P2P_PUSH": "0", "S2_P2P_ONESHOT_MAXW": "4"},  # ... peers pull
+    "many_one_stream": {"S2_CHECK_MANY": "1", "S2_PIPE_STREAMS": "1"},
     "blocks": {"S2_CHECK_NUM_BLOCKS": "62500"},  # block bitmap (b < d, 32 elements per block)
 }
 
