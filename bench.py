@@ -346,15 +346,31 @@ def ours(args, cfg):
     clocks.mark("load_start")
     for i in range(args.warmup):
         step(i)
-    # soak: keep the GPU busy ~0.3 s before timing so clocks settle (extra untimed warm-up)
+    # soak (extra untimed warm-up): keep the GPU busy until clocks and memory power states settle —
+    # at least 0.5 s and until two consecutive 50-step batches agree within 2 % (at most 3 s; a
+    # fresh box's first run once measured 45 % slow after a fixed 0.3 s soak)
     barrier()
     t_soak = time.time()
-    i = 0
-    while time.time() - t_soak < 0.3:
+    i, prev = 0, None
+    sa, sb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    while True:
+        sa.record(stream)
         for _ in range(50):
             step(i)
             i += 1
+        sb.record(stream)
         torch.cuda.synchronize()
+        cur = sa.elapsed_time(sb)
+        settled = prev is not None and abs(cur - prev) <= 0.02 * prev
+        prev = cur
+        done = time.time() - t_soak > 0.5 and settled
+        if world > 1:  # every rank leaves the soak together
+            flag = torch.tensor([0.0 if done or time.time() - t_soak > 3.0 else 1.0], device="cuda")
+            dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+            if flag.item() == 0.0:
+                break
+        elif done or time.time() - t_soak > 3.0:
+            break
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ms_plain = None
