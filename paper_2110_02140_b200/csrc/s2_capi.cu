@@ -670,7 +670,7 @@ static int stage_compress(s2_plan* plan, const float* g, uint64_t* counters, boo
 static int stage_exchange(s2_plan* plan, cudaStream_t st, void* stream, StepBufs* b) {
   b->un = b->bitmap;
   b->dec_table = b->table;
-  b->health = s2::DecodeHealth{nullptr, b->cnt, plan->status};
+  b->health = s2::DecodeHealth{nullptr, b->cnt, plan->status, 0};
   if (plan->world == 1) return S2_OK;
   if (plan->p2p) {
     plan->pa.cur = b->cur;
@@ -753,6 +753,8 @@ int s2_reduce_many(s2_plan* plan, const float* const* gs, float* const* outs, in
     if (!plan->xstream) {
       int lo = 0, hi = 0;
       S2_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi), "stream priorities");
+      // highest priority: exchange CTAs take SMs as the neighbouring kernels' CTAs retire (lowest
+      // priority measured 1-10 % slower per reduce, profiles/r02_ab_pipe_streams.txt)
       S2_CUDA(cudaStreamCreateWithPriority(&plan->xstream, cudaStreamNonBlocking, hi), "exchange stream");
       for (int k = 0; k < s2_plan::kPipeEvents; ++k) {
         S2_CUDA(cudaEventCreateWithFlags(&plan->ev_c[k], cudaEventDisableTiming), "event");
@@ -770,8 +772,9 @@ int s2_reduce_many(s2_plan* plan, const float* const* gs, float* const* outs, in
       S2_CUDA(cudaEventRecord(ex, xs), "record exchange");
       return S2_OK;
     };
-    auto decode = [&](const StepBufs& b, float* out, int k) -> int {
+    auto decode = [&](StepBufs b, float* out, int k) -> int {
       S2_CUDA(cudaStreamWaitEvent(st, plan->ev_x[k % s2_plan::kPipeEvents], 0), "decode waits exchange");
+      b.health.fence_zero = 1;  // the next compress on this stream uses the table it zeroes
       return stage_decode(plan, out, st, b);
     };
     const bool late0 = !overlaps(gs[0], plan->prev_out, nb);
@@ -779,7 +782,9 @@ int s2_reduce_many(s2_plan* plan, const float* const* gs, float* const* outs, in
     if ((rc = exchange(&prev, 0))) return rc;
     plan->step += 1;
     for (int k = 1; k < n; ++k) {
-      if ((rc = stage_compress(plan, gs[k], nullptr, true, st, &cur))) return rc;
+      // compress(1) directly follows compress(0): its table was zeroed by the decode two reduces
+      // back, whose completion only compress(0)'s exit guarantees, so it waits up front
+      if ((rc = stage_compress(plan, gs[k], nullptr, k > 1, st, &cur))) return rc;
       if ((rc = exchange(&cur, k))) return rc;
       if ((rc = decode(prev, outs[k - 1], k - 1))) return rc;
       plan->step += 1;

@@ -32,10 +32,13 @@ cudaError_t launch_compress(const Plan& p, const float* g, uint32_t* bitmap, flo
 // wrong gradient — and `status` (device or mapped pinned host word, or null) receives
 // S2_STATUS_NONFINITE if this rank's compress saw NaN/Inf (counters[S2_CNT_NONFINITE]) and
 // S2_STATUS_EXCHANGE if the exchange timed out.
+// `fence_zero`: fence the prologue's zeroing of the next table before dependents may launch (set
+// when the compress that follows on the stream uses that very table: s2_reduce_many's two streams).
 struct DecodeHealth {
   const uint32_t* poison;
   const unsigned long long* counters;
   uint32_t* status;
+  int fence_zero;
 };
 cudaError_t launch_decode(const Plan& p, const uint32_t* bitmap, const float* table, int workers,
                           float* out, cudaStream_t st, float* zero_table = nullptr,
