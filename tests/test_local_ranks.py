@@ -266,3 +266,28 @@ def test_local_exchange_beside_concurrent_compute(W, push):
             assert np.array_equal(out.cpu().numpy(), ref), (k, r)
     assert words.cpu().tolist() == [0] * W and grp.errors() == [0] * W
     assert torch.isfinite(cs[-1]).all()
+
+
+@pytest.mark.parametrize("W,n", [(2, 1), (2, 2), (4, 2), (4, 3)])
+def test_local_reduce_many_short_batches(W, n):
+    """Batches of 1..3 reduces (the two-stream schedule's first compress waits up front; n = 1 stays
+    on one stream), back to back with single reduces on the same plans, all checked."""
+    import torch
+
+    from paper_2110_02140_b200.local import LocalGroup
+
+    dim, rows, cols = 300_007, 3, 4099
+    grp = LocalGroup(W, dim, rows, cols)
+    host = [[o.synthetic_gradient(dim, 0.01 * (1 + k), r, kind="int", base_seed=13 * k + 1) for r in range(W)]
+            for k in range(n + 1)]
+    outs = grp.reduce_many([[torch.from_numpy(g).cuda() for g in step] for step in host[:n]])
+    single = grp.reduce([torch.from_numpy(g).cuda() for g in host[n]])  # a plain reduce right after the batch
+    again = grp.reduce_many([[torch.from_numpy(g).cuda() for g in step] for step in host[:n]])
+    torch.cuda.synchronize()
+    for k, step in enumerate(host):
+        ref = o.decompress(o.merge([o.compress(g, g != 0, rows, cols, 0) for g in step])).astype(np.float32)
+        got = [single] if k == n else [outs[k], again[k]]
+        for res in got:
+            for r in range(W):
+                assert np.array_equal(res[r].cpu().numpy(), ref), (k, r)
+    assert grp.errors() == [0] * W
