@@ -20,10 +20,13 @@ from paper_2110_02140_b200 import synthetic  # noqa: E402
 from paper_2110_02140_b200._lib import S2_MASK_NONZERO, check, lib, ptr  # noqa: E402
 from paper_2110_02140_b200.sketch import get_plan  # noqa: E402
 
+# argv: compress density [decode union density] (e.g. 0.01 0.04: a W = 4 step's compress and decode)
 cfg = dict(dim=25_600_000, alpha=float(sys.argv[1]) if len(sys.argv) > 1 else 0.01)
+cfg["alpha_d"] = float(sys.argv[2]) if len(sys.argv) > 2 else cfg["alpha"]
 d, rows, cols = cfg["dim"], 3, 262_144
 plan = get_plan(d, d, rows, cols, 0)
-gs = [synthetic.gradient(dict(dim=d, alpha=cfg["alpha"], rows=None), 0, base_seed=1234 + 1000 * k) for k in range(4)]
+gs = [synthetic.gradient(dict(dim=d, alpha=cfg["alpha"] if k < 2 else cfg["alpha_d"], rows=None), 0,
+                         base_seed=1234 + 1000 * k) for k in range(4)]
 outs = [torch.empty(d, device="cuda") for _ in range(4)]
 bms = [torch.empty((d + 31) // 32, dtype=torch.int32, device="cuda") for _ in range(4)]
 tabs = [torch.zeros(rows * cols, device="cuda") for _ in range(4)]
@@ -61,7 +64,7 @@ def timed(fn):
 
 
 cur = torch.cuda.current_stream()
-res = {"alpha": cfg["alpha"]}
+res = {"alpha": cfg["alpha"], "alpha_d": cfg["alpha_d"]}
 res["c_us"] = timed(lambda i: comp(i % 2, cur))
 res["d_us"] = timed(lambda i: dec(2 + i % 2, cur))
 res["seq_us"] = timed(lambda i: (comp(i % 2, cur), dec(2 + i % 2, cur)))
