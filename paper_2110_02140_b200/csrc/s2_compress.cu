@@ -17,7 +17,7 @@
 // The next tile's 8 float4 per lane are loaded into registers before the current tile is
 // processed (127 registers, 2 CTAs = 16 warps per SM); every alternative that puts more
 // bytes in flight (TMA rings, warp-specialised producer, bulk L2 prefetch, extra waves)
-// measured slower (code at git tag r01-variants).
+// measured slower (code at commit 17ff0c0, the last round-1 commit).
 // NaN/Inf are non-zeros, so finiteness is tested on the queue only (MODE 2 tests every
 // element: unselected non-zeros never reach the queue).
 #include "s2_device.cuh"
