@@ -29,4 +29,5 @@ for alpha in (0.10, 0.05, 0.01, 0.001):
             continue
         d = json.loads(lines[-1])
         print(json.dumps({"alpha": alpha, "cols": cols, "gpus": a.gpus, "ms": d["ms_per_step"],
-                          "GBps_total": d["value"], "phases": d["phases"]}), flush=True)
+                          "latency_ms": d.get("latency_ms_per_reduce"), "GBps_per_gpu": d["value"],
+                          "GBps_job": d.get("job_GBps"), "phases": d["phases"]}), flush=True)
