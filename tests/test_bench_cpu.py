@@ -50,3 +50,22 @@ def test_cpu_baseline_reports_as_shipped():
     assert cb["kind"] == "port" and cb["value"] > 0 and cb["cores"] >= 1
     a = cb["as_shipped"]
     assert a["kind"] == "port-as-shipped" and a["cores"] == 1 and 0 < a["value"] < cb["value"]
+
+
+def test_kernel_floors():
+    """bench.kernel_floors: HBM bytes at the peak vs REDs at the L2 RED rate (compress) and vs
+    L1 -> crossbar requests (decode), whichever is larger, with the bound named."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    d, rows, cols = 25_600_000, 3, 262_144
+    wb = 4 * (-(-d // 32))
+    f1 = bench.kernel_floors(d, rows, cols, wb, 256_000, 256_000, 6552.6)
+    assert f1["compress"]["bound"] == "hbm" and f1["decode"]["bound"] == "hbm"
+    assert abs(f1["compress"]["us"] - (4 * d + wb + 4 * rows * cols) / 6552.6e9 * 1e6) < 0.01
+    assert f1["decode"]["requests"] == int(rows * 256_000 + (4 * d + 4 * rows * cols + wb) / 32)
+    f8 = bench.kernel_floors(d, rows, cols, wb, 256_000, int(0.0773 * d), 6552.6)
+    assert f8["decode"]["bound"] == "l1-xbar requests" and f8["decode"]["us"] > f1["decode"]["us"]
+    fb = bench.kernel_floors(110_000_000, 5, 1 << 20, 4 * (110_000_000 // 32), 5_500_000, 5_500_000, 6552.6)
+    assert fb["compress"]["bound"] == "l2 red"
+    assert abs(fb["compress"]["us"] - 5 * 5_500_000 / bench.L2_RED_PER_S * 1e6) < 0.01
