@@ -751,7 +751,7 @@ int s2_reduce_many(s2_plan* plan, const float* const* gs, float* const* outs, in
   if (plan->p2p && n > 1 && streams == 2) {
     // Two streams.  Main: compress(0) compress(1) decode(0) compress(2) decode(1) ... decode(n-1);
     // exchange stream: exchange(0) exchange(1) ..., exchange(k) after compress(k), decode(k) after
-    // exchange(k).  Every exchange (NVLink- and latency-bound, half the SMs, mostly spinning) runs
+    // exchange(k).  Every exchange (NVLink- and latency-bound, a quarter to half of the SMs) runs
     // beside the HBM-bound compress AND decode of the neighbouring reduces, so a batch costs about
     // (compress + decode) per reduce once the exchange is shorter than that.  Buffer safety: table
     // and bitmap slots rotate over 4, union / tsum / inbox over 2; exchange(k+1) touches slots k+1
