@@ -393,18 +393,13 @@ static int sm_count(int* G) {
 // base pointers known: plan tables into the arena, counters, trace, grid, timeout
 static int finish_p2p(s2_plan* plan, int G) {
   s2::P2PArgs& a = plan->pa;
-  // exchange-kernel CTAs (1024 threads each).  W <= 2 (pull one-shot): one per SM, or one per two
-  // SMs when the exchanged table + bitmap is small (<= 8 MB: fewer cross-rank flag pairs, ~1 µs per
-  // step faster at the ResNet-50 config; slower for the 12-56 MB exchanges).  W > 2 (push two-shot):
-  // one per four SMs at every size — the same one-at-a-time latency (W = 4: ResNet-50 80.0 vs
-  // 80.1 µs, BERT 775 vs 767 µs at G/2, 770 at G) and less of the GPU held by spinning CTAs while
-  // s2_reduce_many overlaps the exchange with compress and decode (per reduce ResNet-50 66.0 vs
-  // 70.2 µs, BERT 707 vs 720 / 770 µs; profiles/r02_ab_exchange_grid.txt)
-  const int64_t xbytes = 4 * (a.cells + a.words);
-  if (a.world > 2)
-    plan->p2p_grid = G >= 4 ? G / 4 : 1;
-  else
-    plan->p2p_grid = (xbytes <= (8ll << 20) && G >= 2) ? G / 2 : G;
+  // exchange-kernel CTAs (1024 threads each): one per two SMs at W <= 2 (pull one-shot), one per
+  // four SMs at W > 2 (push two-shot), at every exchange size.  Fewer CTAs cost little or nothing
+  // one reduce at a time and leave more of the GPU to the compress and decode that s2_reduce_many
+  // overlaps with the exchange (profiles/r02_ab_exchange_grid.txt): per reduce W = 4 ResNet-50
+  // 70.2 -> 66.0 µs (one at a time 80.1 / 80.0), BERT 770 (#SMs) -> 707 µs (770 / 775); W = 2
+  // GPT-2-M 99 % 616 (#SMs) -> 577 µs (614 / 617), LSTM 351 -> 329 µs (354 / 362).
+  plan->p2p_grid = a.world > 2 ? (G >= 4 ? G / 4 : 1) : (G >= 2 ? G / 2 : 1);
   const char* ge = getenv("S2_P2P_GRID");  // override (A/B runs)
   if (ge && atoi(ge) > 0 && atoi(ge) <= 8 * G) plan->p2p_grid = atoi(ge);
   if (plan->opt_grid > 0) plan->p2p_grid = plan->opt_grid;
