@@ -8,6 +8,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges cost a few ns unless a profiler is attached
+
 #include "s2.h"
 #include "s2_common.cuh"
 #include "s2_kernels.h"
@@ -58,6 +60,14 @@ struct s2_plan {
 namespace {
 
 thread_local std::string g_err;
+
+// host-side NVTX range over an enqueue (nsys / ncu --nvtx show where each stage was issued)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -656,6 +666,7 @@ static bool overlaps(const void* a, const void* b, size_t n) {
 // compress of step plan->step (slots from the step counter); `late`: may overlap its predecessor
 static int stage_compress(s2_plan* plan, const float* g, uint64_t* counters, bool late, cudaStream_t st,
                           StepBufs* b) {
+  NvtxRange nvtx_("s2 compress");
   b->cur = (int)(plan->step & 1);
   b->tc = (int)(plan->step & 3);
   b->tz = (int)((plan->step + 2) & 3);
@@ -670,6 +681,7 @@ static int stage_compress(s2_plan* plan, const float* g, uint64_t* counters, boo
 }
 
 static int stage_exchange(s2_plan* plan, cudaStream_t st, void* stream, StepBufs* b) {
+  NvtxRange nvtx_("s2 exchange");
   b->un = b->bitmap;
   b->dec_table = b->table;
   b->health = s2::DecodeHealth{nullptr, b->cnt, plan->status, 0};
@@ -690,6 +702,7 @@ static int stage_exchange(s2_plan* plan, cudaStream_t st, void* stream, StepBufs
 }
 
 static int stage_decode(s2_plan* plan, float* out, cudaStream_t st, const StepBufs& b) {
+  NvtxRange nvtx_("s2 decode");
   S2_CUDA(s2::launch_decode(plan->p, b.un, b.dec_table, plan->world, out, st, plan->tables[b.tz],
                             plan->counters[b.tz], &b.health),
           "s2_reduce/decode");
@@ -697,6 +710,7 @@ static int stage_decode(s2_plan* plan, float* out, cudaStream_t st, const StepBu
 }
 
 int s2_reduce(s2_plan* plan, const float* g, float* out, uint64_t* counters, void* stream) {
+  NvtxRange nvtx_("s2_reduce");
   int rc = check_reduce_args(plan, g, out);
   if (rc) return rc;
   cudaStream_t st = as_stream(stream);
@@ -717,6 +731,7 @@ int s2_reduce(s2_plan* plan, const float* g, float* out, uint64_t* counters, voi
 }
 
 int s2_reduce_many(s2_plan* plan, const float* const* gs, float* const* outs, int n, void* stream) {
+  NvtxRange nvtx_("s2_reduce_many");
   if (!plan || n < 0 || (n > 0 && (!gs || !outs))) return fail(S2_EINVAL, "NULL argument to s2_reduce_many");
   if (n == 0) return S2_OK;
   for (int k = 0; k < n; ++k) {
